@@ -1,0 +1,186 @@
+/*
+ * glsim_cuda.h -- C ABI of libglsim_cuda.so, the B200 (sm_100a) engine for the
+ * windowed gate-level re-simulation hot path of GATSPI (arXiv 2203.06117).
+ *
+ * The reference package calls its hot path through four numba kernels in
+ * pkg/src/glsim/_kernels.py, orchestrated by pkg/src/glsim/simcore.py and
+ * report.py.  This library replaces that seam.  Every entry point below names
+ * the reference interface it stands in for (file:line, 1-based).
+ *
+ * Conventions
+ *   - plain pointers and sizes only; all pointers are HOST pointers unless a
+ *     parameter name ends in _dev;
+ *   - integers are the reference's int64 femtoseconds / counts (numpy int64),
+ *     value bits are uint8 (numpy uint8);
+ *   - every function returns a gs_status (0 = ok); gs_last_error() returns a
+ *     thread-local message for the last failure;
+ *   - the caller owns all host memory; handles own their device memory;
+ *   - one engine per device; calls on one engine are not thread-safe.
+ */
+#ifndef GLSIM_CUDA_H
+#define GLSIM_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum gs_status {
+  GS_OK = 0,
+  GS_ERR_ARG = 1,         /* bad argument / unsupported input  -> ValueError        */
+  GS_ERR_CUDA = 2,        /* CUDA runtime failure              -> RuntimeError      */
+  GS_ERR_NODEVICE = 3,    /* no CUDA device visible            -> RuntimeError      */
+  GS_ERR_CAPACITY = 4,    /* device memory cannot hold one tile-> CapacityError     */
+  GS_ERR_CONSISTENCY = 5  /* device-side invariant violated    -> ConsistencyError  */
+} gs_status;
+
+typedef struct gs_design gs_design;
+typedef struct gs_stim gs_stim;
+typedef struct gs_engine gs_engine;
+
+/* Flat design, exactly the arrays of reference CompiledDesign
+ * (pkg/src/glsim/simcore.py:203-272) plus the levelization
+ * (pkg/src/glsim/netlist.py:293-312).  Gate g drives net num_pis + g
+ * (netlist.py:144-149). */
+typedef struct gs_design_desc {
+  int64_t num_pis, num_gates, num_levels;
+  const int64_t *order;        /* [G] gates in level order               */
+  const int64_t *level_starts; /* [L+1] CSR offsets into order           */
+  const int64_t *pin_off;      /* [G+1]                                   */
+  const int64_t *pin_net;      /* [sum k] driving net of each input pin   */
+  const int64_t *pin_ic;       /* [sum k] interconnect delay (fs)         */
+  const int64_t *pin_arc;      /* [sum k] first row of the pin's table    */
+  const int64_t *arc_rows;     /* [R*2] (rise, fall) per condition row    */
+  int64_t num_arc_rows;
+  const int64_t *lut_off;      /* [G] offset of the gate's truth table    */
+  const uint8_t *lut_bits;     /* [sum 2^k]                               */
+  int64_t num_lut_bits;
+} gs_design_desc;
+
+/* Stimulus.  Either the whole-run CSR form (what StimulusSet.build receives,
+ * pkg/src/glsim/waveform.py:243-265; kernel K1 cuts the windows on the GPU)
+ * or the reference's windowed arrays (StimulusSet.__init__, waveform.py:235-241).
+ * Set the pointers of exactly one form; the other form's pointers are NULL. */
+typedef struct gs_stim_desc {
+  int64_t num_pis, num_windows;
+  const int64_t *boundaries;   /* [W+1] strictly ascending window edges    */
+  /* CSR form */
+  const int64_t *pi_off;       /* [P+1]                                    */
+  const int64_t *pi_times;     /* [pi_off[P]] strictly ascending per input  */
+  const uint8_t *pi_init;      /* [P]                                      */
+  /* windowed form */
+  const int64_t *buf;          /* [n_buf] absolute toggle times            */
+  int64_t n_buf;
+  const int64_t *offsets;      /* [P*W]                                    */
+  const int64_t *counts;       /* [P*W]                                    */
+  const uint8_t *initials;     /* [P*W]                                    */
+} gs_stim_desc;
+
+/* Per-net results of a stats run; host arrays the caller allocates. */
+typedef struct gs_stats_out {
+  int64_t *t1;    /* [N] fs at 1 (T0 = duration - T1)        (report.py:82-86)  */
+  int64_t *tc;    /* [N] stored toggles                       (report.py:82-86)  */
+  int64_t *ig;    /* [N] inertially filtered pulses, gates    (report.py:87-89)  */
+  int64_t totals[3]; /* filtered, ic_filtered, discarded      (scheduler.py:70-74)*/
+} gs_stats_out;
+
+/* Per-(gate, window) arrays of one window range, row-major [G, Ws] (pitch Ws);
+ * host arrays the caller allocates; any pointer may be NULL to skip it.
+ * These are the fields of reference WaveformArena (waveform.py:280-303) and
+ * PassResult (simcore.py:286-292). */
+typedef struct gs_arena_out {
+  int64_t *counts, *peak, *filtered, *ic_filtered, *discarded;
+  uint8_t *initials;
+  /* store pass: region offsets [G, Ws] into buf (waveform.py:340-345) and the
+   * buffer itself (absolute int64 fs, sum(caps) entries).  buf != NULL makes
+   * the run a store pass. */
+  const int64_t *offsets;
+  int64_t *buf;
+  int64_t n_buf;
+} gs_arena_out;
+
+/* Timing of the last gs_run (CUDA events on the engine stream). */
+typedef struct gs_timing {
+  float ms_total;        /* all kernels of the run, device time               */
+  float ms_gate_eval;    /* K4 launches only                                  */
+  float ms_stim;         /* K1 launches only                                  */
+  int64_t launches;      /* kernels launched                                  */
+  int64_t gate_eval_launches;
+  int64_t chunks;        /* window chunks the run was split into              */
+  int64_t data_bytes_peak; /* high-water device waveform pool usage            */
+  int64_t input_toggles; /* sum over gate-windows of fanin toggles (n_in)      */
+  int64_t output_toggles;/* stored output toggles                              */
+} gs_timing;
+
+/* ---- library ---------------------------------------------------------- */
+int gs_version(void);
+const char *gs_last_error(void);
+int gs_device_count(int *count);
+
+/* ---- design (replaces CompiledDesign, simcore.py:203-276) ------------- */
+int gs_design_create(const gs_design_desc *desc, int device, gs_design **out);
+int gs_design_destroy(gs_design *d);
+
+/* ---- stimulus (replaces StimulusSet.build / slice_windows,
+ *      waveform.py:49-63,243-265; the cutting itself runs in kernel K1) --- */
+int gs_stim_create(gs_design *d, const gs_stim_desc *desc, gs_stim **out);
+int gs_stim_destroy(gs_stim *s);
+
+/* ---- engine ------------------------------------------------------------ */
+/* mem_budget: bytes of device memory the engine may use for its window-chunk
+ * workspace (0 = 75% of free memory).  stream: a cudaStream_t (NULL = the
+ * engine's own stream). */
+int gs_engine_create(gs_design *d, int64_t mem_budget, void *stream, gs_engine **out);
+int gs_engine_destroy(gs_engine *e);
+
+/* Stats run over windows [w_lo, w_hi): K1 stim_segment + per level K4
+ * gate_eval with the dwell/toggle reduction fused (replaces count_pass +
+ * store_pass + compute_stats: simcore.py:328-410, report.py:57-91,
+ * _kernels.py:17-210,254-295).  Results are ADDED into *out (so window shards
+ * and segments merge by summation, report.py:46-54).  pct = pathpulse percent
+ * (scheduler.py:390). */
+int gs_run_stats(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct,
+                 gs_stats_out *out);
+
+/* Same run writing per-(gate, window) arena arrays for [w_lo, w_hi): a count
+ * pass when arena->buf is NULL (count_pass, simcore.py:328-379, incl. peak),
+ * a store pass into the reference arena layout otherwise (store_pass,
+ * simcore.py:382-410).  stats may be NULL. */
+int gs_run_arena(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct,
+                 gs_arena_out *arena, gs_stats_out *stats);
+
+int gs_last_timing(gs_engine *e, gs_timing *t);
+
+/* Device-side stats accumulation for multi-GPU reduction: like gs_run_stats
+ * but ADDS into a caller-owned device buffer acc_dev of 3*N+3 int64
+ * ([t1 | tc | ig | filtered, ic_filtered, discarded]), so the caller can
+ * all-reduce it with NCCL before one host copy. */
+int gs_run_stats_device(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct,
+                        int64_t *acc_dev);
+
+/* ---- kernel-seam entry points: same arguments as the reference's numba
+ * kernels, host arrays in and out, executed on the GPU ------------------- */
+
+/* dwell_sweep (_kernels.py:254-295): per-net T0/T1/TC over windows
+ * [w_lo, w_hi) of windowed stimulus + arena arrays; ADDS into t0/t1/tc [N].
+ * g_* arrays are [G, Wg] with column = window - w_off. */
+int gs_dwell_sweep(int64_t num_nets, const uint8_t *net_kind, const int64_t *net_slot,
+                   const int64_t *stim_buf, int64_t n_stim_buf,
+                   const int64_t *stim_off, const int64_t *stim_cnt, const uint8_t *stim_init,
+                   int64_t num_pis, int64_t num_windows,
+                   const int64_t *gbuf, int64_t n_gbuf,
+                   const int64_t *g_off, const int64_t *g_cnt, const uint8_t *g_init,
+                   int64_t num_gates, int64_t g_cols,
+                   const int64_t *boundaries, int64_t w_lo, int64_t w_hi, int64_t w_off,
+                   int64_t *t0_out, int64_t *t1_out, int64_t *tc_out);
+
+/* init_values (_kernels.py:213-231): zero-delay window-start value of every
+ * net; vals_out is [num_nets, W] uint8, rows < P copied from stim_init [P, W]. */
+int gs_init_values(const gs_design_desc *desc, const uint8_t *stim_init, int64_t num_windows,
+                   uint8_t *vals_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GLSIM_CUDA_H */

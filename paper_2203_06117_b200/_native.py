@@ -1,0 +1,310 @@
+"""ctypes binding of ``libglsim_cuda.so`` (C ABI in ``include/glsim_cuda.h``).
+
+This is the only door to the GPU.  There is no CPU fallback: if the library is
+missing or no CUDA device is visible, every entry point raises.  Status codes
+map onto the package's error types (``GS_ERR_CAPACITY`` -> ``CapacityError``,
+``GS_ERR_CONSISTENCY`` -> ``ConsistencyError``).
+"""
+
+import ctypes as C
+import os
+import weakref
+
+import numpy as np
+
+from .errors import CapacityError, ConsistencyError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_NAME = "libglsim_cuda.so"
+LIB_PATH = os.path.join(_HERE, LIB_NAME)
+
+GS_OK, GS_ERR_ARG, GS_ERR_CUDA, GS_ERR_NODEVICE, GS_ERR_CAPACITY, GS_ERR_CONSISTENCY = range(6)
+
+_i64p = C.POINTER(C.c_int64)
+_u8p = C.POINTER(C.c_uint8)
+
+
+class DesignDesc(C.Structure):
+    _fields_ = [("num_pis", C.c_int64), ("num_gates", C.c_int64), ("num_levels", C.c_int64),
+                ("order", _i64p), ("level_starts", _i64p), ("pin_off", _i64p),
+                ("pin_net", _i64p), ("pin_ic", _i64p), ("pin_arc", _i64p),
+                ("arc_rows", _i64p), ("num_arc_rows", C.c_int64),
+                ("lut_off", _i64p), ("lut_bits", _u8p), ("num_lut_bits", C.c_int64)]
+
+
+class StimDesc(C.Structure):
+    _fields_ = [("num_pis", C.c_int64), ("num_windows", C.c_int64), ("boundaries", _i64p),
+                ("pi_off", _i64p), ("pi_times", _i64p), ("pi_init", _u8p),
+                ("buf", _i64p), ("n_buf", C.c_int64), ("offsets", _i64p),
+                ("counts", _i64p), ("initials", _u8p)]
+
+
+class StatsOut(C.Structure):
+    _fields_ = [("t1", _i64p), ("tc", _i64p), ("ig", _i64p), ("totals", C.c_int64 * 3)]
+
+
+class ArenaOut(C.Structure):
+    _fields_ = [("counts", _i64p), ("peak", _i64p), ("filtered", _i64p),
+                ("ic_filtered", _i64p), ("discarded", _i64p), ("initials", _u8p),
+                ("offsets", _i64p), ("buf", _i64p), ("n_buf", C.c_int64)]
+
+
+class Timing(C.Structure):
+    _fields_ = [("ms_total", C.c_float), ("ms_gate_eval", C.c_float), ("ms_stim", C.c_float),
+                ("launches", C.c_int64), ("gate_eval_launches", C.c_int64),
+                ("chunks", C.c_int64), ("data_bytes_peak", C.c_int64),
+                ("input_toggles", C.c_int64), ("output_toggles", C.c_int64)]
+
+
+# every symbol include/glsim_cuda.h declares, with its ctypes signature
+SIGNATURES = {
+    "gs_version": (C.c_int, []),
+    "gs_last_error": (C.c_char_p, []),
+    "gs_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "gs_design_create": (C.c_int, [C.POINTER(DesignDesc), C.c_int, C.POINTER(C.c_void_p)]),
+    "gs_design_destroy": (C.c_int, [C.c_void_p]),
+    "gs_stim_create": (C.c_int, [C.c_void_p, C.POINTER(StimDesc), C.POINTER(C.c_void_p)]),
+    "gs_stim_destroy": (C.c_int, [C.c_void_p]),
+    "gs_engine_create": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "gs_engine_destroy": (C.c_int, [C.c_void_p]),
+    "gs_run_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                               C.POINTER(StatsOut)]),
+    "gs_run_arena": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                               C.POINTER(ArenaOut), C.POINTER(StatsOut)]),
+    "gs_last_timing": (C.c_int, [C.c_void_p, C.POINTER(Timing)]),
+    "gs_run_stats_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                                      C.c_void_p]),
+    "gs_dwell_sweep": (C.c_int, [C.c_int64, _u8p, _i64p, _i64p, C.c_int64, _i64p, _i64p, _u8p,
+                                 C.c_int64, C.c_int64, _i64p, C.c_int64, _i64p, _i64p, _u8p,
+                                 C.c_int64, C.c_int64, _i64p, C.c_int64, C.c_int64, C.c_int64,
+                                 _i64p, _i64p, _i64p]),
+    "gs_init_values": (C.c_int, [C.POINTER(DesignDesc), _u8p, C.c_int64, _u8p]),
+}
+
+_lib = None
+
+
+def load(path=LIB_PATH):
+    """Load the library (once).  Raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{LIB_NAME} is not built ({path} missing); run "
+                           "`python -c 'import __graft_entry__ as g; g.build()'` first. "
+                           "There is no CPU fallback.")
+    lib = C.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(rc):
+    if rc == GS_OK:
+        return
+    msg = (_lib.gs_last_error() or b"").decode(errors="replace")
+    if rc == GS_ERR_CAPACITY:
+        raise CapacityError(f"device memory: {msg}")
+    if rc == GS_ERR_CONSISTENCY:
+        raise ConsistencyError(msg)
+    if rc == GS_ERR_ARG:
+        raise ValueError(msg)
+    raise RuntimeError(f"libglsim_cuda: {msg}")
+
+
+def _p64(a):
+    return a.ctypes.data_as(_i64p) if a is not None else None
+
+
+def _p8(a):
+    return a.ctypes.data_as(_u8p) if a is not None else None
+
+
+def _c64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _c8(a):
+    return np.ascontiguousarray(a, dtype=np.uint8)
+
+
+def device_count():
+    lib = load()
+    n = C.c_int(0)
+    _check(lib.gs_device_count(C.byref(n)))
+    return n.value
+
+
+_device = None
+
+
+def current_device():
+    """Device index this process drives: ``set_device`` > ``LOCAL_RANK`` > 0."""
+    if _device is not None:
+        return _device
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def set_device(i):
+    global _device
+    _device = int(i)
+
+
+def _design_desc(m):
+    keep = dict(order=_c64(m.order), level_starts=_c64(m.level_starts), pin_off=_c64(m.pin_off),
+                pin_net=_c64(m.pin_net), pin_ic=_c64(m.pin_ic), pin_arc=_c64(m.pin_arc),
+                arc_rows=_c64(m.arc_rows).reshape(-1), lut_off=_c64(m.lut_off),
+                lut_bits=_c8(m.lut_bits))
+    d = DesignDesc(num_pis=m.num_pis, num_gates=m.num_gates, num_levels=m.num_levels,
+                   order=_p64(keep["order"]), level_starts=_p64(keep["level_starts"]),
+                   pin_off=_p64(keep["pin_off"]), pin_net=_p64(keep["pin_net"]),
+                   pin_ic=_p64(keep["pin_ic"]), pin_arc=_p64(keep["pin_arc"]),
+                   arc_rows=_p64(keep["arc_rows"]), num_arc_rows=keep["arc_rows"].size // 2,
+                   lut_off=_p64(keep["lut_off"]), lut_bits=_p8(keep["lut_bits"]),
+                   num_lut_bits=keep["lut_bits"].size)
+    return d, keep
+
+
+class Design:
+    """Device copy of a compiled design (``gs_design``)."""
+
+    def __init__(self, model, device=None):
+        lib = load()
+        self.device = current_device() if device is None else device
+        desc, keep = _design_desc(model)
+        h = C.c_void_p()
+        _check(lib.gs_design_create(C.byref(desc), self.device, C.byref(h)))
+        self.handle = h
+        self.num_nets = model.num_pis + model.num_gates
+        self.num_pis = model.num_pis
+        self.num_gates = model.num_gates
+        self._fin = weakref.finalize(self, lib.gs_design_destroy, h)
+
+
+class Stimulus:
+    """Device copy of a stimulus set (``gs_stim``), CSR or windowed form."""
+
+    def __init__(self, design, stimuli):
+        lib = load()
+        b = _c64(stimuli.boundaries)
+        keep = {"b": b}
+        d = StimDesc(num_pis=stimuli.num_pis, num_windows=b.size - 1, boundaries=_p64(b))
+        if stimuli.is_csr:
+            keep.update(off=_c64(stimuli.pi_off), t=_c64(stimuli.pi_times), i=_c8(stimuli.pi_init))
+            d.pi_off, d.pi_times, d.pi_init = _p64(keep["off"]), _p64(keep["t"]), _p8(keep["i"])
+        else:
+            keep.update(buf=_c64(stimuli.buf), off=_c64(stimuli.offsets),
+                        cnt=_c64(stimuli.counts), ini=_c8(stimuli.initials))
+            d.buf, d.n_buf = _p64(keep["buf"]), keep["buf"].size
+            d.offsets, d.counts = _p64(keep["off"]), _p64(keep["cnt"])
+            d.initials = _p8(keep["ini"])
+        h = C.c_void_p()
+        _check(lib.gs_stim_create(design.handle, C.byref(d), C.byref(h)))
+        self.handle = h
+        self.design = design
+        self.num_windows = b.size - 1
+        self._fin = weakref.finalize(self, lib.gs_stim_destroy, h)
+
+
+class Engine:
+    """Per-device engine (``gs_engine``): chunk workspace, stream, timers."""
+
+    def __init__(self, design, mem_budget=0, stream=None):
+        lib = load()
+        h = C.c_void_p()
+        _check(lib.gs_engine_create(design.handle, int(mem_budget),
+                                    C.c_void_p(stream) if stream else None, C.byref(h)))
+        self.handle = h
+        self.design = design
+        self._fin = weakref.finalize(self, lib.gs_engine_destroy, h)
+
+    def run_stats(self, stim, w_lo, w_hi, pct):
+        """Stats over [w_lo, w_hi): (t1, tc, ig [N] int64, totals (filt, icf, disc))."""
+        N = self.design.num_nets
+        t1, tc, ig = (np.zeros(N, dtype=np.int64) for _ in range(3))
+        out = StatsOut(t1=_p64(t1), tc=_p64(tc), ig=_p64(ig))
+        _check(load().gs_run_stats(self.handle, stim.handle, int(w_lo), int(w_hi), int(pct),
+                                   C.byref(out)))
+        return t1, tc, ig, tuple(int(x) for x in out.totals)
+
+    def run_stats_device(self, stim, w_lo, w_hi, pct, acc_ptr):
+        """Add stats of [w_lo, w_hi) into a device int64 buffer [3N+3] at acc_ptr."""
+        _check(load().gs_run_stats_device(self.handle, stim.handle, int(w_lo), int(w_hi),
+                                          int(pct), C.c_void_p(acc_ptr)))
+
+    def run_arena(self, stim, w_lo, w_hi, pct, offsets=None, n_buf=0, want_stats=False):
+        """Count pass (offsets None) or store pass over [w_lo, w_hi).
+
+        Returns dict of [G, Ws] arrays (counts, peak, filtered, ic_filtered,
+        discarded, initials), ``buf`` for a store pass, and ``stats`` (as
+        :meth:`run_stats`) when requested.
+        """
+        G = self.design.num_gates
+        Ws = int(w_hi) - int(w_lo)
+        res = {k: np.zeros((G, Ws), dtype=np.int64)
+               for k in ("counts", "peak", "filtered", "ic_filtered", "discarded")}
+        res["initials"] = np.zeros((G, Ws), dtype=np.uint8)
+        a = ArenaOut(counts=_p64(res["counts"]), peak=_p64(res["peak"]),
+                     filtered=_p64(res["filtered"]), ic_filtered=_p64(res["ic_filtered"]),
+                     discarded=_p64(res["discarded"]), initials=_p8(res["initials"]))
+        if offsets is not None:
+            off = _c64(offsets)
+            buf = np.empty(int(n_buf), dtype=np.int64)
+            res["buf"] = buf
+            a.offsets, a.buf, a.n_buf = _p64(off), (_p64(buf) if buf.size else
+                                                    C.cast(C.c_void_p(8), _i64p)), buf.size
+        st = None
+        if want_stats:
+            N = self.design.num_nets
+            t1, tc, ig = (np.zeros(N, dtype=np.int64) for _ in range(3))
+            st = StatsOut(t1=_p64(t1), tc=_p64(tc), ig=_p64(ig))
+        _check(load().gs_run_arena(self.handle, stim.handle, int(w_lo), int(w_hi), int(pct),
+                                   C.byref(a), C.byref(st) if st is not None else None))
+        if want_stats:
+            res["stats"] = (t1, tc, ig, tuple(int(x) for x in st.totals))
+        return res
+
+    def timing(self):
+        t = Timing()
+        _check(load().gs_last_timing(self.handle, C.byref(t)))
+        return {f: getattr(t, f) for f, _ in Timing._fields_}
+
+
+def dwell_sweep(arena, stimuli, boundaries, num_pis, num_gates):
+    """GPU dwell_sweep (``_kernels.py:254-295``) over an arena: per-net (t1, tc, ig)."""
+    lib = load()
+    N = num_pis + num_gates
+    net_kind = np.zeros(N, dtype=np.uint8)
+    net_kind[num_pis:] = 1
+    net_slot = np.concatenate([np.arange(num_pis), np.arange(num_gates)]).astype(np.int64)
+    w_lo, w_hi = arena.window_range
+    sbuf, soff, scnt, sini = (_c64(stimuli.buf), _c64(stimuli.offsets), _c64(stimuli.counts),
+                              _c8(stimuli.initials))
+    gbuf, goff, gcnt, gini = (_c64(arena.buf), _c64(arena.offsets), _c64(arena.counts),
+                              _c8(arena.initials))
+    b = _c64(boundaries)
+    t0, t1, tc = (np.zeros(N, dtype=np.int64) for _ in range(3))
+    W = b.size - 1
+    _check(lib.gs_dwell_sweep(N, _p8(net_kind), _p64(net_slot), _p64(sbuf), sbuf.size,
+                              _p64(soff), _p64(scnt), _p8(sini), num_pis, W,
+                              _p64(gbuf), gbuf.size, _p64(goff), _p64(gcnt), _p8(gini),
+                              num_gates, goff.shape[1] if goff.ndim == 2 else w_hi - w_lo,
+                              _p64(b), w_lo, w_hi, w_lo, _p64(t0), _p64(t1), _p64(tc)))
+    ig = np.zeros(N, dtype=np.int64)
+    if num_gates:
+        ig[num_pis:] = np.asarray(arena.filtered, dtype=np.int64).sum(axis=1)
+    return t1, tc, ig
+
+
+def init_values(model, stim_init):
+    """GPU init_values (``_kernels.py:213-231``): uint8 [N, W]."""
+    lib = load()
+    desc, keep = _design_desc(model)
+    si = _c8(stim_init)
+    W = si.shape[1] if si.ndim == 2 else 0
+    out = np.zeros((model.num_pis + model.num_gates, W), dtype=np.uint8)
+    _check(lib.gs_init_values(C.byref(desc), _p8(si), W, _p8(out)))
+    return out

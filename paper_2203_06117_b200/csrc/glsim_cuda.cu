@@ -1,0 +1,954 @@
+// glsim_cuda.cu -- host engine and C ABI of libglsim_cuda.so (see include/glsim_cuda.h).
+//
+// One engine per device.  A run walks its window range in chunks sized to the
+// device memory budget; per chunk it launches K1 (stimulus segmentation) and
+// then one K4 launch per logic level (the level barrier), all on one stream,
+// and synchronizes once at the chunk end to check the device-side flags.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "glsim_cuda.h"
+#include "kernels.cuh"
+
+using namespace gs;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      (void)cudaGetLastError();                                                         \
+      return fail(e_ == cudaErrorMemoryAllocation ? GS_ERR_CAPACITY : GS_ERR_CUDA,      \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                  \
+    }                                                                                   \
+  } while (0)
+
+#define TRY(call)               \
+  do {                                     \
+    int rc_ = (call);                      \
+    if (rc_ != GS_OK) return rc_;          \
+  } while (0)
+
+template <typename T>
+int dalloc(T **p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaMalloc((void **)p, n * sizeof(T)));
+  return GS_OK;
+}
+
+template <typename T>
+void dfree(T *&p) {
+  if (p) cudaFree((void *)p);
+  p = nullptr;
+}
+
+template <typename T>
+int upload(T **p, const T *src, size_t n) {
+  TRY(dalloc(p, n));
+  if (n) CK(cudaMemcpy(*p, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  return GS_OK;
+}
+
+int use_device(int dev) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    (void)cudaGetLastError();
+    return fail(GS_ERR_NODEVICE, "no CUDA device visible");
+  }
+  if (dev < 0 || dev >= n) return fail(GS_ERR_ARG, "device index out of range");
+  CK(cudaSetDevice(dev));
+  return GS_OK;
+}
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+}  // namespace
+
+// =========================================================================
+// design
+
+struct gs_design {
+  int device = 0;
+  int P = 0, G = 0, N = 0, L = 0;
+  std::vector<int64_t> level_starts;
+  std::vector<int> n_small;          // per level: gates with k <= 4 (ordered first)
+  std::vector<int64_t> fanout;       // per net: input pins it drives
+  std::vector<int> k_of;             // per gate
+  int64_t sum_k = 0;
+  int *order = nullptr, *gate_k = nullptr, *gate_pin = nullptr, *pin_net = nullptr,
+      *pin_arc = nullptr;
+  long long *pin_ic = nullptr, *arc = nullptr;
+  unsigned long long *gate_lut = nullptr;
+  unsigned *lut_words = nullptr;
+
+  DesignDev dev() const {
+    DesignDev D;
+    D.P = P;
+    D.G = G;
+    D.N = N;
+    D.order = order;
+    D.gate_k = gate_k;
+    D.gate_pin = gate_pin;
+    D.gate_lut = gate_lut;
+    D.lut_words = lut_words;
+    D.pin_net = pin_net;
+    D.pin_ic = pin_ic;
+    D.pin_arc = pin_arc;
+    D.arc = arc;
+    return D;
+  }
+  void release() {
+    dfree(order); dfree(gate_k); dfree(gate_pin); dfree(pin_net); dfree(pin_arc);
+    dfree(pin_ic); dfree(arc); dfree(gate_lut); dfree(lut_words);
+  }
+};
+
+static int design_build(const gs_design_desc *d, int device, gs_design *D) {
+  if (!d) return fail(GS_ERR_ARG, "null design descriptor");
+  const int64_t P = d->num_pis, G = d->num_gates, L = d->num_levels;
+  if (P < 0 || G < 0 || L < 0 || P + G > INT32_MAX)
+    return fail(GS_ERR_ARG, "design size out of range");
+  if (G > 0 && (!d->order || !d->level_starts || !d->pin_off || !d->lut_off || !d->lut_bits))
+    return fail(GS_ERR_ARG, "missing design arrays");
+  D->device = device;
+  D->P = (int)P;
+  D->G = (int)G;
+  D->N = (int)(P + G);
+  D->L = (int)L;
+  const int64_t N = P + G;
+  // ---- validation (a bad index must never reach the device)
+  std::vector<int> level_of(G, -1);
+  D->level_starts.assign(d->level_starts, d->level_starts + (L + 1));
+  if (D->level_starts[0] != 0 || D->level_starts[L] != G)
+    return fail(GS_ERR_ARG, "level_starts must span [0, G]");
+  for (int64_t l = 0; l < L; ++l) {
+    if (D->level_starts[l + 1] < D->level_starts[l])
+      return fail(GS_ERR_ARG, "level_starts not monotone");
+    for (int64_t i = D->level_starts[l]; i < D->level_starts[l + 1]; ++i) {
+      const int64_t g = d->order[i];
+      if (g < 0 || g >= G || level_of[g] >= 0) return fail(GS_ERR_ARG, "order is not a permutation");
+      level_of[g] = (int)l;
+    }
+  }
+  if (G && d->pin_off[0] != 0) return fail(GS_ERR_ARG, "pin_off[0] must be 0");
+  D->k_of.resize(G);
+  D->fanout.assign(N, 0);
+  int64_t n_pins = G ? d->pin_off[G] : 0;
+  if (n_pins > INT32_MAX || d->num_arc_rows > INT32_MAX / 2)
+    return fail(GS_ERR_ARG, "design too large for 32-bit pin/arc indices");
+  for (int64_t g = 0; g < G; ++g) {
+    const int64_t k = d->pin_off[g + 1] - d->pin_off[g];
+    if (k < 1 || k > kMaxK) return fail(GS_ERR_ARG, "gate fanin count must be in [1, 16]");
+    D->k_of[g] = (int)k;
+    if (d->lut_off[g] < 0 || d->lut_off[g] + (int64_t(1) << k) > d->num_lut_bits)
+      return fail(GS_ERR_ARG, "lut_off out of range");
+    for (int64_t p = d->pin_off[g]; p < d->pin_off[g + 1]; ++p) {
+      const int64_t n = d->pin_net[p];
+      if (n < 0 || n >= N) return fail(GS_ERR_ARG, "pin_net out of range");
+      if (n >= P && level_of[n - P] >= level_of[g])
+        return fail(GS_ERR_ARG, "fanin is not on an earlier level");
+      if (d->pin_ic[p] < 0) return fail(GS_ERR_ARG, "negative interconnect delay");
+      if (d->pin_arc[p] < 0 || d->pin_arc[p] + (int64_t(1) << (k - 1)) > d->num_arc_rows)
+        return fail(GS_ERR_ARG, "pin_arc out of range");
+      D->fanout[n] += 1;
+    }
+  }
+  for (int64_t r = 0; r < 2 * d->num_arc_rows; ++r)
+    if (d->arc_rows[r] < 0) return fail(GS_ERR_ARG, "negative arc delay");
+  D->sum_k = n_pins;
+
+  // ---- device order: per level, k <= 4 gates first (fast kernel), then k > 4
+  std::vector<int> order(G);
+  D->n_small.assign(L, 0);
+  for (int64_t l = 0; l < L; ++l) {
+    int64_t o = D->level_starts[l];
+    for (int pass = 0; pass < 2; ++pass)
+      for (int64_t i = D->level_starts[l]; i < D->level_starts[l + 1]; ++i) {
+        const int64_t g = d->order[i];
+        if ((D->k_of[g] <= 4) == (pass == 0)) {
+          order[o++] = (int)g;
+          if (pass == 0) D->n_small[l] += 1;
+        }
+      }
+  }
+  std::vector<int> gate_pin(G);
+  std::vector<unsigned long long> gate_lut(G);
+  std::vector<unsigned> words;
+  for (int64_t g = 0; g < G; ++g) {
+    const int k = D->k_of[g];
+    gate_pin[g] = (int)d->pin_off[g];
+    const uint8_t *t = d->lut_bits + d->lut_off[g];
+    if (k <= 6) {
+      unsigned long long m = 0;
+      for (int i = 0; i < (1 << k); ++i) m |= (unsigned long long)(t[i] & 1u) << i;
+      gate_lut[g] = m;
+    } else {
+      gate_lut[g] = words.size();
+      const int nw = (1 << k) / 32;
+      for (int w = 0; w < nw; ++w) {
+        unsigned m = 0;
+        for (int b = 0; b < 32; ++b) m |= (unsigned)(t[w * 32 + b] & 1u) << b;
+        words.push_back(m);
+      }
+    }
+  }
+  std::vector<int> pin_net(n_pins), pin_arc(n_pins);
+  for (int64_t p = 0; p < n_pins; ++p) {
+    pin_net[p] = (int)d->pin_net[p];
+    pin_arc[p] = (int)d->pin_arc[p];
+  }
+  TRY(use_device(device));
+  TRY(upload(&D->order, order.data(), G));
+  TRY(upload(&D->gate_k, D->k_of.data(), G));
+  TRY(upload(&D->gate_pin, gate_pin.data(), G));
+  TRY(upload(&D->gate_lut, gate_lut.data(), G));
+  TRY(upload(&D->lut_words, words.data(), words.size()));
+  TRY(upload(&D->pin_net, pin_net.data(), n_pins));
+  TRY(upload(&D->pin_arc, pin_arc.data(), n_pins));
+  TRY(upload(&D->pin_ic, (const long long *)d->pin_ic, n_pins));
+  TRY(upload(&D->arc, (const long long *)d->arc_rows, 2 * d->num_arc_rows));
+  return GS_OK;
+}
+
+// =========================================================================
+// stimulus
+
+struct gs_stim {
+  gs_design *d = nullptr;
+  int P = 0;
+  int64_t W = 0;
+  bool csr = true, wide = false;
+  std::vector<int64_t> bnd_host;
+  int64_t n_toggles = 0;
+  long long *bnd = nullptr, *pi_off = nullptr, *pi_times = nullptr, *buf = nullptr,
+            *offsets = nullptr, *counts = nullptr;
+  unsigned char *pi_init = nullptr, *initials = nullptr;
+
+  StimDev dev() const {
+    StimDev S;
+    S.P = P;
+    S.W = W;
+    S.pi_off = pi_off;
+    S.pi_times = pi_times;
+    S.pi_init = pi_init;
+    S.buf = buf;
+    S.offsets = offsets;
+    S.counts = counts;
+    S.nbuf = n_toggles;
+    S.initials = initials;
+    return S;
+  }
+  void release() {
+    dfree(bnd); dfree(pi_off); dfree(pi_times); dfree(buf); dfree(offsets); dfree(counts);
+    dfree(pi_init); dfree(initials);
+  }
+};
+
+static int stim_build(gs_design *D, const gs_stim_desc *s, gs_stim *S) {
+  if (!s || !s->boundaries) return fail(GS_ERR_ARG, "null stimulus descriptor");
+  if (s->num_pis != D->P) return fail(GS_ERR_ARG, "stimulus input count != design inputs");
+  if (s->num_windows < 1) return fail(GS_ERR_ARG, "need at least one window");
+  S->d = D;
+  S->P = (int)s->num_pis;
+  S->W = s->num_windows;
+  S->bnd_host.assign(s->boundaries, s->boundaries + s->num_windows + 1);
+  int64_t maxlen = 0;
+  for (int64_t w = 0; w < S->W; ++w) {
+    const int64_t len = S->bnd_host[w + 1] - S->bnd_host[w];
+    if (len <= 0) return fail(GS_ERR_ARG, "window boundaries must be strictly ascending");
+    maxlen = std::max(maxlen, len);
+  }
+  S->wide = maxlen > (int64_t)0xFFFFFFFFll;
+  S->csr = s->pi_off != nullptr;
+  TRY(use_device(D->device));
+  TRY(upload(&S->bnd, (const long long *)s->boundaries, S->W + 1));
+  const int64_t P = S->P, W = S->W;
+  if (S->csr) {
+    if (!s->pi_times || !s->pi_init) return fail(GS_ERR_ARG, "incomplete CSR stimulus");
+    if (s->pi_off[0] != 0) return fail(GS_ERR_ARG, "pi_off[0] must be 0");
+    for (int64_t p = 0; p < P; ++p) {
+      if (s->pi_off[p + 1] < s->pi_off[p]) return fail(GS_ERR_ARG, "pi_off not monotone");
+      for (int64_t i = s->pi_off[p] + 1; i < s->pi_off[p + 1]; ++i)
+        if (s->pi_times[i] <= s->pi_times[i - 1])
+          return fail(GS_ERR_ARG, "input toggle times must be strictly increasing");
+    }
+    S->n_toggles = s->pi_off[P];
+    TRY(upload(&S->pi_off, (const long long *)s->pi_off, P + 1));
+    TRY(upload(&S->pi_times, (const long long *)s->pi_times, S->n_toggles));
+    TRY(upload(&S->pi_init, s->pi_init, P));
+  } else {
+    if (!s->buf && s->n_buf) return fail(GS_ERR_ARG, "missing stimulus buffer");
+    if (!s->offsets || !s->counts || !s->initials) return fail(GS_ERR_ARG, "incomplete windowed stimulus");
+    for (int64_t i = 0; i < P * W; ++i) {
+      if (s->counts[i] < 0 || s->offsets[i] < 0 || s->offsets[i] + s->counts[i] > s->n_buf)
+        return fail(GS_ERR_ARG, "stimulus window region out of range");
+      const int64_t w = i % W;
+      for (int64_t j = 0; j < s->counts[i]; ++j) {
+        const int64_t t = s->buf[s->offsets[i] + j];
+        if (t < S->bnd_host[w] || t >= S->bnd_host[w + 1] ||
+            (j && t <= s->buf[s->offsets[i] + j - 1]))
+          return fail(GS_ERR_ARG, "stimulus toggle outside its window or not increasing");
+      }
+    }
+    S->n_toggles = s->n_buf;
+    TRY(upload(&S->buf, (const long long *)s->buf, s->n_buf));
+    TRY(upload(&S->offsets, (const long long *)s->offsets, P * W));
+    TRY(upload(&S->counts, (const long long *)s->counts, P * W));
+    TRY(upload(&S->initials, s->initials, P * W));
+  }
+  return GS_OK;
+}
+
+// =========================================================================
+// engine
+
+struct gs_engine {
+  gs_design *d = nullptr;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  int sms = 0;
+  int64_t budget = 0;
+  // chunk workspace
+  int64_t meta_windows = 0;          // capacity (windows, multiple of 32)
+  unsigned *cnt = nullptr;
+  unsigned long long *tbase = nullptr;
+  unsigned *init = nullptr;
+  void *data = nullptr;
+  int64_t data_bytes = 0;
+  int64_t pool_bytes = 0;            // requested gate-pool bytes
+  int ncta_cap = 0;
+  unsigned long long *bump = nullptr;
+  long long *acc = nullptr, *acc_run = nullptr;
+  int *err = nullptr, *err_host = nullptr;
+  unsigned long long *bump_host = nullptr;
+  // arena workspace
+  int64_t arena_windows = 0;
+  long long *a_cnt = nullptr, *a_peak = nullptr, *a_filt = nullptr, *a_icf = nullptr,
+            *a_disc = nullptr, *a_off = nullptr, *a_buf = nullptr;
+  unsigned char *a_init = nullptr;
+  int64_t a_buf_cap = 0;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t chunk_hint = 0;
+  gs_timing last{};
+
+  void release_meta() { dfree(cnt); dfree(tbase); dfree(init); meta_windows = 0; }
+  void release_arena() {
+    dfree(a_cnt); dfree(a_peak); dfree(a_filt); dfree(a_icf); dfree(a_disc); dfree(a_off);
+    dfree(a_init); arena_windows = 0;
+  }
+  void release() {
+    release_meta();
+    release_arena();
+    dfree(a_buf);
+    dfree(data);
+    dfree(bump);
+    dfree(acc);
+    dfree(acc_run);
+    dfree(err);
+    if (err_host) cudaFreeHost(err_host);
+    if (bump_host) cudaFreeHost(bump_host);
+    err_host = nullptr;
+    bump_host = nullptr;
+    for (auto &e : ev)
+      if (e) cudaEventDestroy(e), e = nullptr;
+    if (own_stream && st) cudaStreamDestroy(st);
+    st = nullptr;
+  }
+};
+
+namespace {
+
+template <typename TS, int MODE>
+int grid_size(gs_engine *e, int *ncta) {
+  int a = 0, b = 0, c = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, gate_eval<TS, MODE, false>, kEvalThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, gate_eval<TS, MODE, true>, kEvalThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, stim_segment_win<TS>, kEvalThreads, 0));
+  int occ = std::max(1, std::min(a, std::min(b, c)));
+  *ncta = e->sms * occ;
+  return GS_OK;
+}
+
+// ensure per-chunk metadata arrays hold `wins` windows
+int ensure_meta(gs_engine *e, int64_t wins) {
+  if (e->meta_windows >= wins) return GS_OK;
+  e->release_meta();
+  const int64_t N = e->d->N;
+  const int64_t Wpad = round_up(wins, kWarp);
+  TRY(dalloc(&e->cnt, (size_t)(N * Wpad)));
+  TRY(dalloc(&e->tbase, (size_t)(N * (Wpad / kWarp))));
+  TRY(dalloc(&e->init, (size_t)(N * (Wpad / kWarp))));
+  e->meta_windows = Wpad;
+  return GS_OK;
+}
+
+int ensure_arena(gs_engine *e, int64_t wins, bool store) {
+  if (e->arena_windows >= wins && (!store || e->a_off)) return GS_OK;
+  e->release_arena();
+  const size_t n = (size_t)e->d->G * (size_t)round_up(wins, kWarp);
+  TRY(dalloc(&e->a_cnt, n));
+  TRY(dalloc(&e->a_peak, n));
+  TRY(dalloc(&e->a_filt, n));
+  TRY(dalloc(&e->a_icf, n));
+  TRY(dalloc(&e->a_disc, n));
+  TRY(dalloc(&e->a_init, n));
+  TRY(dalloc(&e->a_off, n));
+  e->arena_windows = round_up(wins, kWarp);
+  return GS_OK;
+}
+
+int ensure_data(gs_engine *e, int64_t bytes) {
+  if (e->data_bytes >= bytes) return GS_OK;
+  dfree(e->data);
+  e->data_bytes = 0;
+  CK(cudaMalloc(&e->data, (size_t)bytes));
+  e->data_bytes = bytes;
+  return GS_OK;
+}
+
+int64_t meta_bytes_per_window(const gs_design *d, bool arena) {
+  int64_t b = (int64_t)d->N * 4 + (int64_t)d->N * 12 / kWarp + 1;
+  if (arena) b += (int64_t)d->G * (6 * 8 + 1);
+  return b;
+}
+
+struct RunOut {
+  long long *acc_dev;       // [3N+3] device accumulators results are added to
+  gs_arena_out *arena;      // may be null
+  int64_t w_base;           // first window of the arena's column range
+  int64_t arena_cols;       // Ws (host row pitch)
+};
+
+template <typename TS, int MODE>
+int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, RunOut &ro) {
+  gs_design *D = e->d;
+  const int64_t N = D->N, G = D->G;
+  const bool arena = MODE != MODE_STATS;
+  const bool store = MODE == MODE_STORE;
+  int ncta = 0;
+  TRY((grid_size<TS, MODE>(e, &ncta)));
+  if (ncta > e->ncta_cap) {
+    dfree(e->bump);
+    if (e->bump_host) cudaFreeHost(e->bump_host);
+    e->bump_host = nullptr;
+    TRY(dalloc(&e->bump, ncta));
+    CK(cudaMallocHost((void **)&e->bump_host, sizeof(unsigned long long) * ncta));
+    e->ncta_cap = ncta;
+  }
+  const int64_t per_win = meta_bytes_per_window(D, arena);
+  const int64_t pi_words = s->csr ? s->n_toggles : 0;
+  const int64_t pi_bytes = round_up(pi_words * (int64_t)sizeof(TS), 256);
+  const int64_t total = w_hi - w_lo;
+  // initial chunk: metadata takes at most ~40% of the budget
+  int64_t Wc = e->chunk_hint > 0 ? e->chunk_hint
+                                  : std::max<int64_t>(kWarp, (e->budget * 2 / 5) / per_win);
+  Wc = std::min<int64_t>(Wc, round_up(total, kWarp));
+  Wc = std::max<int64_t>(kWarp, Wc / kWarp * kWarp);
+  const double density = (s->P && s->W) ? (double)s->n_toggles / ((double)s->P * s->W) : 0.0;
+
+  if (store) {
+    if (ro.arena->n_buf > e->a_buf_cap) {
+      dfree(e->a_buf);
+      e->a_buf_cap = 0;
+      TRY(dalloc(&e->a_buf, (size_t)ro.arena->n_buf));
+      e->a_buf_cap = ro.arena->n_buf;
+    }
+  }
+
+  const DesignDev Dd = D->dev();
+  const StimDev Sd = s->dev();
+  int64_t w = w_lo;
+  float ms_stim = 0.f, ms_eval = 0.f, ms_total = 0.f;
+  int64_t launches = 0, eval_launches = 0, chunks = 0, peak_bytes = 0;
+  int64_t pool_bytes = e->pool_bytes;
+  while (w < w_hi) {
+    const int64_t wc = std::min<int64_t>(Wc, w_hi - w);
+    const int64_t Wpad = round_up(wc, kWarp);
+    const int Tc = (int)(Wpad / kWarp);
+    TRY(ensure_meta(e, Wpad));
+    if (arena) TRY(ensure_arena(e, Wpad, store));
+    // gate pool: generous estimate of stored toggles, at least 64 MiB
+    const int64_t meta_now = per_win * Wpad;
+    int64_t room = e->budget - meta_now - pi_bytes;
+    if (room < (int64_t)ncta * 4096) {
+      if (Wc > kWarp) { Wc = std::max<int64_t>(kWarp, Wc / 2 / kWarp * kWarp); continue; }
+      return fail(GS_ERR_CAPACITY, "device memory budget cannot hold one 32-window chunk");
+    }
+    const double est_words = (double)G * wc * std::max(2.0, 4.0 * density) * 2.0;
+    int64_t want = std::max<int64_t>(pool_bytes, std::max<int64_t>(64ll << 20,
+                                     (int64_t)(est_words * sizeof(TS))));
+    want = std::min(want, room);
+    TRY(ensure_data(e, pi_bytes + want));
+    const int64_t pool_words = (e->data_bytes - pi_bytes) / (int64_t)sizeof(TS);
+    const int64_t part_words = pool_words / ncta;
+
+    ChunkDev C;
+    memset(&C, 0, sizeof(C));
+    C.N = (int)N;
+    C.Wc = (int)wc;
+    C.Tc = Tc;
+    C.Wpad = (int)Wpad;
+    C.w0 = w;
+    C.bnd = s->bnd;
+    C.cnt = e->cnt;
+    C.tbase = e->tbase;
+    C.init = e->init;
+    C.data = e->data;
+    C.pool_base = (unsigned long long)(pi_bytes / (int64_t)sizeof(TS));
+    C.part_words = (unsigned long long)part_words;
+    C.bump = e->bump;
+    C.acc = e->acc;
+    C.err = e->err;
+    if (arena) {
+      C.a_cnt = e->a_cnt;
+      C.a_peak = e->a_peak;
+      C.a_filt = e->a_filt;
+      C.a_icf = e->a_icf;
+      C.a_disc = e->a_disc;
+      C.a_init = e->a_init;
+      C.a_off = e->a_off;
+      C.a_buf = e->a_buf;
+      C.a_nbuf = store ? ro.arena->n_buf : 0;
+      if (store) {
+        CK(cudaMemcpy2DAsync(e->a_off, Wpad * 8, ro.arena->offsets + (w - ro.w_base),
+                             ro.arena_cols * 8, wc * 8, G, cudaMemcpyHostToDevice, e->st));
+      }
+    }
+    CK(cudaMemsetAsync(e->acc, 0, sizeof(long long) * ACC_ROWS * N, e->st));
+    CK(cudaMemsetAsync(e->bump, 0, sizeof(unsigned long long) * ncta, e->st));
+    CK(cudaMemsetAsync(e->err, 0, sizeof(int) * ERR_NFLAGS, e->st));
+    CK(cudaEventRecord(e->ev[0], e->st));
+    // ---- K1
+    int k1 = 0;
+    if (s->P > 0) {
+      const int tpi = std::max(1, std::min(Tc, 8));
+      const int ntg = (Tc + tpi - 1) / tpi;
+      const int64_t items = (int64_t)s->P * ntg;
+      if (s->csr) {
+        const int blocks = (int)std::min<int64_t>((items + 7) / 8, (int64_t)e->sms * 16);
+        stim_segment_csr<TS><<<blocks, 256, 0, e->st>>>(Sd, C, tpi, ntg);
+      } else {
+        stim_segment_win<TS><<<ncta, kEvalThreads, 0, e->st>>>(Sd, C, tpi, ntg);
+      }
+      CK(cudaGetLastError());
+      k1 = 1;
+    }
+    CK(cudaEventRecord(e->ev[1], e->st));
+    // ---- K4, one launch per level (kernel boundary = level barrier)
+    const int64_t warps = (int64_t)ncta * kEvalWarps;
+    int nl = 0;
+    for (int l = 0; l < D->L; ++l) {
+      const int lo = (int)D->level_starts[l];
+      const int n_all = (int)(D->level_starts[l + 1] - D->level_starts[l]);
+      const int n_small = D->n_small[l];
+      for (int part = 0; part < 2; ++part) {
+        const int n = part == 0 ? n_small : n_all - n_small;
+        if (n <= 0) continue;
+        LevelArgs A;
+        A.lo = part == 0 ? lo : lo + n_small;
+        A.n = n;
+        A.tpi = (int)std::max<int64_t>(1, std::min<int64_t>(32, (int64_t)n * Tc / (8 * warps)));
+        A.tpi = std::min(A.tpi, Tc);
+        A.ntg = (Tc + A.tpi - 1) / A.tpi;
+        A.pct = pct;
+        if (part == 0)
+          gate_eval<TS, MODE, false><<<ncta, kEvalThreads, 0, e->st>>>(Dd, C, A);
+        else
+          gate_eval<TS, MODE, true><<<ncta, kEvalThreads, 0, e->st>>>(Dd, C, A);
+        CK(cudaGetLastError());
+        ++nl;
+      }
+    }
+    CK(cudaEventRecord(e->ev[2], e->st));
+    CK(cudaMemcpyAsync(e->err_host, e->err, sizeof(int) * ERR_NFLAGS, cudaMemcpyDeviceToHost, e->st));
+    CK(cudaMemcpyAsync(e->bump_host, e->bump, sizeof(unsigned long long) * ncta,
+                       cudaMemcpyDeviceToHost, e->st));
+    CK(cudaStreamSynchronize(e->st));
+    if (e->err_host[ERR_CAP])
+      return fail(GS_ERR_CONSISTENCY, "gate output overran its staging bound or arena region "
+                                      "(device-side two-pass invariant violated)");
+    if (e->err_host[ERR_POOL]) {
+      // the chunk did not fit its output regions: grow the pool, else shrink the chunk
+      if (e->data_bytes - pi_bytes < room) {
+        pool_bytes = std::min<int64_t>(room, (e->data_bytes - pi_bytes) * 4);
+      } else if (Wc > kWarp) {
+        Wc = std::max<int64_t>(kWarp, (wc / 2) / kWarp * kWarp);
+      } else {
+        return fail(GS_ERR_CAPACITY, "one 32-window chunk's waveforms exceed the device budget");
+      }
+      continue;
+    }
+    unsigned long long used = 0;
+    for (int c = 0; c < ncta; ++c) used = std::max(used, e->bump_host[c]);
+    peak_bytes = std::max<int64_t>(peak_bytes, (int64_t)(used * ncta * sizeof(TS)) + pi_bytes);
+    float a = 0.f, b = 0.f;
+    CK(cudaEventElapsedTime(&a, e->ev[0], e->ev[1]));
+    CK(cudaEventElapsedTime(&b, e->ev[1], e->ev[2]));
+    ms_stim += a;
+    ms_eval += b;
+    ms_total += a + b;
+    launches += k1 + nl;
+    eval_launches += nl;
+    ++chunks;
+    // ---- results of the chunk
+    {
+      const int threads = 256;
+      const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((N + threads - 1) / threads, 4096));
+      acc_commit<<<blocks, threads, 0, e->st>>>(e->acc, ro.acc_dev, (int)N);
+      CK(cudaGetLastError());
+    }
+    if (arena && ro.arena) {
+      gs_arena_out *ar = ro.arena;
+      const int64_t col = w - ro.w_base;
+      const int64_t dp = ro.arena_cols * 8;
+      struct { int64_t *h; long long *d; } rows[] = {{ar->counts, e->a_cnt}, {ar->peak, e->a_peak},
+          {ar->filtered, e->a_filt}, {ar->ic_filtered, e->a_icf}, {ar->discarded, e->a_disc}};
+      for (auto &r : rows)
+        if (r.h && G)
+          CK(cudaMemcpy2DAsync(r.h + col, dp, r.d, Wpad * 8, wc * 8, G, cudaMemcpyDeviceToHost, e->st));
+      if (ar->initials && G)
+        CK(cudaMemcpy2DAsync(ar->initials + col, ro.arena_cols, e->a_init, Wpad, wc, G,
+                             cudaMemcpyDeviceToHost, e->st));
+      CK(cudaStreamSynchronize(e->st));
+    }
+    // adapt: aim the next chunk at ~60% of the measured per-CTA region fill
+    if (used > 0) {
+      const double fill = (double)used / (double)part_words;
+      if (fill < 0.3 && wc == Wc) Wc = std::min<int64_t>(round_up(total, kWarp), Wc * 2);
+    }
+    w += wc;
+  }
+  e->pool_bytes = pool_bytes;
+  e->chunk_hint = Wc;
+  if (store && ro.arena->n_buf)
+    CK(cudaMemcpyAsync(ro.arena->buf, e->a_buf, sizeof(long long) * ro.arena->n_buf,
+                       cudaMemcpyDeviceToHost, e->st));
+  CK(cudaStreamSynchronize(e->st));
+  e->last.ms_total = ms_total;
+  e->last.ms_gate_eval = ms_eval;
+  e->last.ms_stim = ms_stim;
+  e->last.launches = launches;
+  e->last.gate_eval_launches = eval_launches;
+  e->last.chunks = chunks;
+  e->last.data_bytes_peak = peak_bytes;
+  return GS_OK;
+}
+
+template <int MODE>
+int run_mode(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, RunOut &ro) {
+  if (s->wide) return run_chunks<unsigned long long, MODE>(e, s, w_lo, w_hi, pct, ro);
+  return run_chunks<unsigned, MODE>(e, s, w_lo, w_hi, pct, ro);
+}
+
+int check_run(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct) {
+  if (!e || !s) return fail(GS_ERR_ARG, "null engine or stimulus");
+  if (s->d != e->d) return fail(GS_ERR_ARG, "stimulus belongs to another design");
+  if (w_lo < 0 || w_hi > s->W || w_lo > w_hi) return fail(GS_ERR_ARG, "window range out of bounds");
+  if (pct < 0 || pct > 100) return fail(GS_ERR_ARG, "pathpulse_pct must be within [0, 100]");
+  TRY(use_device(e->d->device));
+  return GS_OK;
+}
+
+int finish_stats(gs_engine *e, gs_stats_out *out) {
+  const int64_t N = e->d->N;
+  std::vector<long long> h(3 * N + 3);
+  CK(cudaMemcpy(h.data(), e->acc_run, sizeof(long long) * (3 * N + 3), cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < N; ++i) {
+    if (out->t1) out->t1[i] += h[i];
+    if (out->tc) out->tc[i] += h[N + i];
+    if (out->ig) out->ig[i] += h[2 * N + i];
+  }
+  for (int j = 0; j < 3; ++j) out->totals[j] += h[3 * N + j];
+  // stored toggles and fanin toggles (sum over pins of the driver's count),
+  // the two data-dependent terms of the algorithmic byte count
+  long long outs = 0, ins = 0;
+  for (int64_t n = 0; n < N; ++n) {
+    if (n >= e->d->P) outs += h[N + n];
+    ins += h[N + n] * e->d->fanout[n];
+  }
+  e->last.output_toggles = outs;
+  e->last.input_toggles = ins;
+  return GS_OK;
+}
+
+}  // namespace
+
+// =========================================================================
+// C ABI
+
+extern "C" {
+
+int gs_version(void) { return 1; }
+
+const char *gs_last_error(void) { return g_err.c_str(); }
+
+int gs_device_count(int *count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    n = 0;
+  }
+  if (count) *count = n;
+  return GS_OK;
+}
+
+int gs_design_create(const gs_design_desc *desc, int device, gs_design **out) {
+  if (!out) return fail(GS_ERR_ARG, "null output handle");
+  *out = nullptr;
+  gs_design *D = new gs_design();
+  int rc = design_build(desc, device, D);
+  if (rc != GS_OK) {
+    D->release();
+    delete D;
+    return rc;
+  }
+  *out = D;
+  return GS_OK;
+}
+
+int gs_design_destroy(gs_design *d) {
+  if (!d) return GS_OK;
+  cudaSetDevice(d->device);
+  d->release();
+  delete d;
+  return GS_OK;
+}
+
+int gs_stim_create(gs_design *d, const gs_stim_desc *desc, gs_stim **out) {
+  if (!d || !out) return fail(GS_ERR_ARG, "null design or output handle");
+  *out = nullptr;
+  gs_stim *S = new gs_stim();
+  int rc = stim_build(d, desc, S);
+  if (rc != GS_OK) {
+    S->release();
+    delete S;
+    return rc;
+  }
+  *out = S;
+  return GS_OK;
+}
+
+int gs_stim_destroy(gs_stim *s) {
+  if (!s) return GS_OK;
+  cudaSetDevice(s->d->device);
+  s->release();
+  delete s;
+  return GS_OK;
+}
+
+int gs_engine_create(gs_design *d, int64_t mem_budget, void *stream, gs_engine **out) {
+  if (!d || !out) return fail(GS_ERR_ARG, "null design or output handle");
+  *out = nullptr;
+  TRY(use_device(d->device));
+  gs_engine *e = new gs_engine();
+  e->d = d;
+  int rc = [&]() -> int {
+    CK(cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, d->device));
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    e->budget = mem_budget > 0 ? mem_budget : (int64_t)(fr * 3 / 4);
+    if (stream) {
+      e->st = (cudaStream_t)stream;
+    } else {
+      CK(cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking));
+      e->own_stream = true;
+    }
+    for (auto &ev : e->ev) CK(cudaEventCreate(&ev));
+    TRY(dalloc(&e->acc, (size_t)ACC_ROWS * d->N));
+    TRY(dalloc(&e->acc_run, (size_t)3 * d->N + 3));
+    TRY(dalloc(&e->err, ERR_NFLAGS));
+    CK(cudaMallocHost((void **)&e->err_host, sizeof(int) * ERR_NFLAGS));
+    return GS_OK;
+  }();
+  if (rc != GS_OK) {
+    e->release();
+    delete e;
+    return rc;
+  }
+  *out = e;
+  return GS_OK;
+}
+
+int gs_engine_destroy(gs_engine *e) {
+  if (!e) return GS_OK;
+  cudaSetDevice(e->d->device);
+  cudaStreamSynchronize(e->st);
+  e->release();
+  delete e;
+  return GS_OK;
+}
+
+int gs_run_stats_device(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct,
+                        int64_t *acc_dev) {
+  TRY(check_run(e, s, w_lo, w_hi, pct));
+  if (!acc_dev) return fail(GS_ERR_ARG, "null device accumulator");
+  RunOut ro{(long long *)acc_dev, nullptr, w_lo, w_hi - w_lo};
+  return run_mode<MODE_STATS>(e, s, w_lo, w_hi, pct, ro);
+}
+
+int gs_run_stats(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, gs_stats_out *out) {
+  TRY(check_run(e, s, w_lo, w_hi, pct));
+  if (!out) return fail(GS_ERR_ARG, "null stats output");
+  CK(cudaMemsetAsync(e->acc_run, 0, sizeof(long long) * (3 * (size_t)e->d->N + 3), e->st));
+  RunOut ro{e->acc_run, nullptr, w_lo, w_hi - w_lo};
+  TRY(run_mode<MODE_STATS>(e, s, w_lo, w_hi, pct, ro));
+  return finish_stats(e, out);
+}
+
+int gs_run_arena(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct,
+                 gs_arena_out *arena, gs_stats_out *stats) {
+  TRY(check_run(e, s, w_lo, w_hi, pct));
+  if (!arena) return fail(GS_ERR_ARG, "null arena output");
+  const bool store = arena->buf != nullptr;
+  if (store) {
+    if (!arena->offsets) return fail(GS_ERR_ARG, "store pass needs region offsets");
+    const int64_t G = e->d->G, Ws = w_hi - w_lo;
+    for (int64_t i = 0; i < G * Ws; ++i)
+      if (arena->offsets[i] < 0 || arena->offsets[i] > arena->n_buf)
+        return fail(GS_ERR_ARG, "arena offsets out of range");
+  }
+  CK(cudaMemsetAsync(e->acc_run, 0, sizeof(long long) * (3 * (size_t)e->d->N + 3), e->st));
+  RunOut ro{e->acc_run, arena, w_lo, w_hi - w_lo};
+  if (store) TRY(run_mode<MODE_STORE>(e, s, w_lo, w_hi, pct, ro));
+  else TRY(run_mode<MODE_COUNTERS>(e, s, w_lo, w_hi, pct, ro));
+  if (stats) return finish_stats(e, stats);
+  return GS_OK;
+}
+
+int gs_last_timing(gs_engine *e, gs_timing *t) {
+  if (!e || !t) return fail(GS_ERR_ARG, "null argument");
+  *t = e->last;
+  return GS_OK;
+}
+
+int gs_dwell_sweep(int64_t num_nets, const uint8_t *net_kind, const int64_t *net_slot,
+                   const int64_t *stim_buf, int64_t n_stim_buf, const int64_t *stim_off,
+                   const int64_t *stim_cnt, const uint8_t *stim_init, int64_t num_pis,
+                   int64_t num_windows, const int64_t *gbuf, int64_t n_gbuf, const int64_t *g_off,
+                   const int64_t *g_cnt, const uint8_t *g_init, int64_t num_gates, int64_t g_cols,
+                   const int64_t *boundaries, int64_t w_lo, int64_t w_hi, int64_t w_off,
+                   int64_t *t0_out, int64_t *t1_out, int64_t *tc_out) {
+  if (num_nets < 0 || w_lo < 0 || w_hi > num_windows || w_lo > w_hi || w_lo < w_off ||
+      w_hi - w_off > g_cols)
+    return fail(GS_ERR_ARG, "dwell_sweep: bad sizes or window range");
+  // bounds of every region the kernel will read
+  for (int64_t n = 0; n < num_nets; ++n) {
+    const int64_t s = net_slot[n];
+    const bool pi = net_kind[n] == 0;
+    if (s < 0 || s >= (pi ? num_pis : num_gates)) return fail(GS_ERR_ARG, "dwell_sweep: bad net slot");
+    for (int64_t w = w_lo; w < w_hi; ++w) {
+      const int64_t o = pi ? stim_off[s * num_windows + w] : g_off[s * g_cols + (w - w_off)];
+      const int64_t c = pi ? stim_cnt[s * num_windows + w] : g_cnt[s * g_cols + (w - w_off)];
+      if (o < 0 || c < 0 || o + c > (pi ? n_stim_buf : n_gbuf))
+        return fail(GS_ERR_ARG, "dwell_sweep: waveform region out of range");
+    }
+  }
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  TRY(use_device(dev));
+  DwellArgs A;
+  memset(&A, 0, sizeof(A));
+  unsigned char *nk = nullptr, *si = nullptr, *gi = nullptr;
+  long long *ns = nullptr, *sb = nullptr, *so = nullptr, *sc = nullptr, *gb = nullptr,
+            *go = nullptr, *gc = nullptr, *bd = nullptr, *out = nullptr;
+  int rc = [&]() -> int {
+    TRY(upload(&nk, net_kind, num_nets));
+    TRY(upload(&ns, (const long long *)net_slot, num_nets));
+    TRY(upload(&sb, (const long long *)stim_buf, n_stim_buf));
+    TRY(upload(&so, (const long long *)stim_off, num_pis * num_windows));
+    TRY(upload(&sc, (const long long *)stim_cnt, num_pis * num_windows));
+    TRY(upload(&si, stim_init, num_pis * num_windows));
+    TRY(upload(&gb, (const long long *)gbuf, n_gbuf));
+    TRY(upload(&go, (const long long *)g_off, num_gates * g_cols));
+    TRY(upload(&gc, (const long long *)g_cnt, num_gates * g_cols));
+    TRY(upload(&gi, g_init, num_gates * g_cols));
+    TRY(upload(&bd, (const long long *)boundaries, num_windows + 1));
+    TRY(dalloc(&out, (size_t)3 * num_nets));
+    CK(cudaMemset(out, 0, sizeof(long long) * 3 * (num_nets ? num_nets : 1)));
+    A.N = (int)num_nets;
+    A.net_kind = nk;
+    A.net_slot = ns;
+    A.sbuf = sb;
+    A.soff = so;
+    A.scnt = sc;
+    A.sinit = si;
+    A.sW = num_windows;
+    A.gbuf = gb;
+    A.goff = go;
+    A.gcnt = gc;
+    A.ginit = gi;
+    A.gW = g_cols;
+    A.bnd = bd;
+    A.w_lo = w_lo;
+    A.w_hi = w_hi;
+    A.w_off = w_off;
+    A.t0 = out;
+    A.t1 = out + num_nets;
+    A.tc = out + 2 * num_nets;
+    if (num_nets && w_hi > w_lo) {
+      const int64_t warps = num_nets * ((w_hi - w_lo + 31) / 32);
+      const int blocks = (int)std::min<int64_t>((warps + 7) / 8, 148 * 32);
+      dwell_arena<<<blocks, 256>>>(A);
+      CK(cudaGetLastError());
+    }
+    std::vector<long long> h(3 * num_nets);
+    if (num_nets) CK(cudaMemcpy(h.data(), out, sizeof(long long) * 3 * num_nets, cudaMemcpyDeviceToHost));
+    for (int64_t n = 0; n < num_nets; ++n) {
+      t0_out[n] += h[n];
+      t1_out[n] += h[num_nets + n];
+      tc_out[n] += h[2 * num_nets + n];
+    }
+    return GS_OK;
+  }();
+  dfree(nk); dfree(ns); dfree(sb); dfree(so); dfree(sc); dfree(si); dfree(gb); dfree(go);
+  dfree(gc); dfree(gi); dfree(bd); dfree(out);
+  return rc;
+}
+
+int gs_init_values(const gs_design_desc *desc, const uint8_t *stim_init, int64_t num_windows,
+                   uint8_t *vals_out) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  gs_design D;
+  int rc = design_build(desc, dev, &D);
+  if (rc != GS_OK) {
+    D.release();
+    return rc;
+  }
+  const int64_t N = D.N, W = num_windows;
+  unsigned char *vals = nullptr;
+  rc = [&]() -> int {
+    TRY(dalloc(&vals, (size_t)(N * W)));
+    if (D.P && W) CK(cudaMemcpy(vals, stim_init, (size_t)D.P * W, cudaMemcpyHostToDevice));
+    const DesignDev Dd = D.dev();
+    for (int l = 0; l < D.L; ++l) {
+      const int lo = (int)D.level_starts[l], n = (int)(D.level_starts[l + 1] - lo);
+      const int64_t tot = (int64_t)n * W;
+      if (!tot) continue;
+      const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 16);
+      zero_delay_level<<<blocks, 256>>>(Dd, vals, W, lo, n);
+      CK(cudaGetLastError());
+    }
+    if (N * W) CK(cudaMemcpy(vals_out, vals, (size_t)(N * W), cudaMemcpyDeviceToHost));
+    return GS_OK;
+  }();
+  dfree(vals);
+  D.release();
+  return rc;
+}
+
+}  // extern "C"

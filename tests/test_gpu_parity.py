@@ -1,0 +1,215 @@
+"""GPU parity: the CUDA engine (through the public API and the C ABI) against
+the reference's own outputs (golden fixtures) and the CPU oracle.
+
+Bar: bit-exact on every integer array -- arena buffer, offsets, capacities,
+counts, window-start values, filter/discard counters, per-net T0/T1/TC/IG --
+and byte-identical SAIF.
+"""
+
+import numpy as np
+import pytest
+
+import gen
+import paper_2203_06117_b200 as api
+from paper_2203_06117_b200 import simcore
+from paper_2203_06117_b200.waveform import StimulusSet
+from conftest import golden_names, load_golden
+
+pytestmark = pytest.mark.gpu
+
+ARENA_FIELDS = ("buf", "offsets", "caps", "counts", "pass1_counts", "initials", "filtered",
+                "ic_filtered", "discarded")
+
+
+def gpu_run(docs, **cfg):
+    nl, lv, delays, waves, duration, b, stim = gen.load(docs, api)
+    arena, diag = api.run(lv, stim, delays,
+                          api.RunConfig(mem_cap=None, pathpulse_pct=docs.pct, **cfg))
+    stats = api.compute_stats(arena, stim)
+    return nl, lv, delays, stim, arena, diag, stats
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_arena_and_stats_match_reference(name):
+    docs, ref = load_golden(name)
+    nl, lv, delays, stim, arena, diag, stats = gpu_run(docs)
+    for f in ARENA_FIELDS:
+        assert np.array_equal(getattr(arena, f), ref[f]), f"{name}: arena.{f}"
+    for f in ("t0", "t1", "tc", "ig"):
+        assert np.array_equal(getattr(stats, f), ref[f]), f"{name}: stats.{f}"
+    assert api.write_saif(stats, nl.name) == ref["saif"]
+    rep = api.run_report(stats, diag)
+    for k, v in ref["report"].items():
+        assert rep[k] == v, f"{name}: report[{k}]"
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_streaming_stats_match_reference(name):
+    docs, ref = load_golden(name)
+    nl, lv, delays, waves, duration, b, stim = gen.load(docs, api)
+    model = api.compile_design(lv, delays)
+    stats, diag = api.simulate_streaming(model, stim, api.RunConfig(pathpulse_pct=docs.pct))
+    for f in ("t0", "t1", "tc", "ig"):
+        assert np.array_equal(getattr(stats, f), ref[f]), f"{name}: {f}"
+    assert api.write_saif(stats, nl.name) == ref["saif"]
+    assert diag["discarded"] == ref["report"]["discarded_events"]
+    assert diag["ic_filtered"] == ref["report"]["interconnect_filtered"]
+    assert diag["filtered"] == ref["report"]["total_filtered"]
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_instances_match_oracle(oracle_lib, seed):
+    pct = (100, 0, 50, 100, 90, 100)[seed % 6]
+    docs = gen.make_docs(5000 + seed, n_gates=int(200 + 150 * seed), windows=8 + 9 * seed,
+                         max_toggles=40 + 30 * seed, duration_ps=4000 + 2500 * seed, pct=pct,
+                         max_levels=4 + seed)
+    nl, lv, delays, stim, arena, diag, stats = gpu_run(docs)
+    waves = gen.load(docs, api)[3]
+    d, st, oa, os_ = oracle_lib.simulate(lv, delays, gen.oracle_inputs(nl, waves),
+                                         stim.boundaries, pct=docs.pct, threads=4)
+    for f in ("buf", "offsets", "caps", "counts", "initials", "filtered", "ic_filtered",
+              "discarded"):
+        assert np.array_equal(getattr(arena, f), oa[f]), f"seed {seed}: arena.{f}"
+    for f in ("t0", "t1", "tc", "ig"):
+        assert np.array_equal(getattr(stats, f), os_[f]), f"seed {seed}: {f}"
+
+
+def test_windowed_stimulus_form_matches_csr():
+    # a StimulusSet built from the reference's windowed arrays goes through the
+    # windowed K1 variant; results must equal the CSR (K1 segmentation) path
+    docs, ref = load_golden("many_windows")
+    nl, lv, delays, waves, duration, b, stim = gen.load(docs, api)
+    win = StimulusSet(b, stim.buf.copy(), stim.offsets.copy(), stim.counts.copy(),
+                      stim.initials.copy(), stim.duration)
+    assert not win.is_csr
+    arena, _ = api.run(lv, win, delays, api.RunConfig(mem_cap=None))
+    for f in ARENA_FIELDS:
+        assert np.array_equal(getattr(arena, f), ref[f]), f
+
+
+def test_chunked_run_equals_single_chunk(monkeypatch):
+    # a tiny device budget forces many window chunks (and pool regrowth);
+    # windows are independent, so every array must come out identical
+    docs, ref = load_golden("many_windows")
+    monkeypatch.setattr(simcore, "ENGINE_MEM_BUDGET", 96 << 20)
+    simcore._Session._cache.clear()
+    nl, lv, delays, stim, arena, diag, stats = gpu_run(docs)
+    for f in ARENA_FIELDS:
+        assert np.array_equal(getattr(arena, f), ref[f]), f
+    for f in ("t0", "t1", "tc", "ig"):
+        assert np.array_equal(getattr(stats, f), ref[f]), f
+    simcore._Session._cache.clear()
+
+
+def test_window_subranges_merge_to_full_run():
+    docs, ref = load_golden("many_windows")
+    nl, lv, delays, waves, duration, b, stim = gen.load(docs, api)
+    model = api.compile_design(lv, delays)
+    W = stim.num_windows
+    parts = [(0, 7), (7, 40), (40, 41), (41, W)]
+    total = None
+    for lo, hi in parts:
+        s, _ = api.simulate_streaming(model, stim, window_range=(lo, hi))
+        total = s if total is None else total.merge(s)
+    for f in ("t0", "t1", "tc", "ig"):
+        assert np.array_equal(getattr(total, f), ref[f]), f
+    assert total.duration == int(ref["duration"])
+
+
+def test_empty_stimulus_and_single_inverter():
+    lib = api.parse_library('{"cells":[{"name":"INV","inputs":["A"],"output":"Y","truth":"10"}]}')
+    nl = api.parse_netlist('{"name":"o","inputs":["p0"],"outputs":["z"],"gates":'
+                           '[{"name":"u","cell":"INV","pins":{"A":"p0","Y":"z"}}]}', lib)
+    lv = api.levelize(nl)
+    stim = StimulusSet.build({"p0": api.Waveform(0, [])}, nl, [0, 100])
+    arena = api.two_pass_simulate(lv, stim, api.zero_delays(nl))
+    assert arena.buf.size == 0 and not arena.counts.any()
+    stim = StimulusSet.build({"p0": api.Waveform(0, [40])}, nl, [0, 100])
+    arena = api.two_pass_simulate(lv, stim, api.zero_delays(nl))
+    assert arena.caps[0, 0] == 1
+    assert arena.waveform(0, 0) == api.Waveform(1, [40])
+
+
+def test_narrow_pulses_fully_filtered():
+    # reference acceptance criterion 4 (test_acceptance.py:113-136)
+    lib = api.parse_library('{"cells":[{"name":"BUF","inputs":["A"],"output":"Y","truth":"01"}]}')
+    nl = api.parse_netlist('{"name":"p","inputs":["a"],"outputs":["y"],"gates":'
+                           '[{"name":"u","cell":"BUF","pins":{"A":"a","Y":"y"}}]}', lib)
+    lv = api.levelize(nl)
+    dl = api.zero_delays(nl)
+    dl.tables[0][0][:] = [[5000, 5000]]
+    rng = np.random.default_rng(99)
+    t, times = 1, []
+    for _ in range(1000):
+        w = int(rng.integers(1, 5000))
+        times += [t, t + w]
+        t += w + int(rng.integers(5001, 20000))
+    stim = StimulusSet.build({"a": api.Waveform(0, np.array(times))}, nl, [0, t + 10_000])
+    arena = api.two_pass_simulate(lv, stim, dl)
+    stats = api.compute_stats(arena, stim)
+    assert int(arena.counts.sum()) == 0 and int(stats.ig[nl.net_index["y"]]) == 1000
+
+
+def test_window_joint_discard_keeps_settled_value():
+    # reference test_report.py:133-150: an edge past the window end is dropped,
+    # the next window opens at the zero-delay settled value
+    lib = api.parse_library('{"cells":[{"name":"BUF","inputs":["A"],"output":"Y","truth":"01"}]}')
+    nl = api.parse_netlist('{"name":"b","inputs":["a"],"outputs":[],"gates":'
+                           '[{"name":"u","cell":"BUF","pins":{"A":"a","Y":"y"}}]}', lib)
+    lv = api.levelize(nl)
+    d = api.zero_delays(nl)
+    d.tables[0][0][:] = [[30, 30]]
+    stim = StimulusSet.build({"a": api.Waveform(0, [40])}, nl, [0, 50, 100])
+    arena = api.two_pass_simulate(lv, stim, d)
+    assert arena.waveform(0, 0).times.size == 0 and int(arena.discarded[0, 0]) == 1
+    assert arena.waveform(0, 1).initial == 1
+    back, _ = api.parse_vcd(api.write_vcd(arena, ["y"]), api.parse_netlist(
+        '{"name":"t","inputs":["y"],"outputs":[],"gates":[]}', lib))
+    assert back["y"] == api.Waveform(0, [50])
+
+
+def test_zero_delay_degenerates_to_collapsed_evaluation():
+    # reference acceptance criterion 7: with no delays every output toggles
+    # exactly where its zero-delay value changes
+    for seed in range(6):
+        docs = gen.make_docs(700 + seed, with_sdf=False, windows=3)
+        nl, lv, delays, stim, arena, diag, stats = gpu_run(docs)
+        assert int(arena.filtered.sum()) == 0
+        for w in range(stim.num_windows):
+            pieces = [stim.window_waveform(p, w) for p in range(nl.num_pis)]
+            ts = np.unique(np.concatenate([x.times for x in pieces] + [np.zeros(0, np.int64)]))
+            vals = np.zeros((nl.num_nets, ts.size + 1), dtype=np.uint8)
+            for p, x in enumerate(pieces):
+                vals[p, 0] = x.initial
+                vals[p, 1:] = x.initial ^ (np.searchsorted(x.times, ts, side="right") & 1)
+            for g in lv.order:
+                gate = nl.gates[g]
+                idx = sum(vals[n].astype(np.int64) << p for p, n in enumerate(gate.pin_nets))
+                vals[gate.out_net] = gate.cell.truth[idx]
+            for g in range(nl.num_gates):
+                v = vals[nl.num_pis + g]
+                assert np.array_equal(arena.waveform(g, w).times, ts[v[1:] != v[:-1]])
+
+
+def test_event_queue_simulator_agrees_with_engine():
+    # the independent event-queue simulator (reference oracle.py semantics)
+    from paper_2203_06117_b200 import eventsim
+    for seed in range(8):
+        docs = gen.make_docs(900 + seed, pct=(100, 50)[seed % 2], avg=seed % 3 == 2)
+        nl, lv, delays, stim, arena, diag, stats = gpu_run(docs)
+        for w in range(stim.num_windows):
+            waves = eventsim.oracle_simulate(lv, delays,
+                                             [stim.window_waveform(p, w) for p in range(nl.num_pis)],
+                                             int(stim.boundaries[w + 1]), pathpulse_pct=docs.pct)
+            assert eventsim.compare_waveforms(arena, waves, w, nl) is None
+
+
+def test_c_abi_init_values_matches_oracle(oracle_lib):
+    docs, ref = load_golden("rnd09")
+    nl, lv, delays, waves, duration, b, stim = gen.load(docs, api)
+    model = api.compile_design(lv, delays)
+    vals = simcore.initial_values(model, stim)
+    d = oracle_lib.Design(lv, delays)
+    st = oracle_lib.Stimulus(gen.oracle_inputs(nl, waves), b)
+    assert np.array_equal(vals, oracle_lib.init_values(d, st))
+    assert np.array_equal(vals[nl.num_pis:], ref["initials"])
