@@ -6,6 +6,8 @@ counts, window-start values, filter/discard counters, per-net T0/T1/TC/IG --
 and byte-identical SAIF.
 """
 
+import json
+
 import numpy as np
 import pytest
 
@@ -38,7 +40,7 @@ def test_arena_and_stats_match_reference(name):
     for f in ("t0", "t1", "tc", "ig"):
         assert np.array_equal(getattr(stats, f), ref[f]), f"{name}: stats.{f}"
     assert api.write_saif(stats, nl.name) == ref["saif"]
-    rep = api.run_report(stats, diag)
+    rep = json.loads(json.dumps(api.run_report(stats, diag)))
     for k, v in ref["report"].items():
         assert rep[k] == v, f"{name}: report[{k}]"
 
