@@ -108,6 +108,28 @@ class Design:
                 self.net_kind[n] = 1
                 self.net_slot[n] = n - P
 
+    @classmethod
+    def from_arrays(cls, num_pis, order, level_starts, pin_off, pin_net, pin_ic, pin_arc,
+                    arc_rows, lut_off, lut_bits):
+        """Flat arrays given directly (array-native synthetic designs); gate g
+        drives net num_pis + g."""
+        self = cls.__new__(cls)
+        c64 = lambda a: np.ascontiguousarray(a, dtype=np.int64)  # noqa: E731
+        self.num_pis = int(num_pis)
+        self.num_gates = len(pin_off) - 1
+        self.num_nets = self.num_pis + self.num_gates
+        self.order, self.level_starts = c64(order), c64(level_starts)
+        self.pin_off, self.pin_net, self.pin_ic = c64(pin_off), c64(pin_net), c64(pin_ic)
+        self.pin_arc, self.arc_rows = c64(pin_arc), c64(arc_rows).reshape(-1, 2)
+        self.lut_off = c64(lut_off)
+        self.lut_bits = np.ascontiguousarray(lut_bits, dtype=np.uint8)
+        self.out_net = np.arange(self.num_pis, self.num_nets, dtype=np.int64)
+        self.net_kind = np.zeros(self.num_nets, dtype=np.uint8)
+        self.net_kind[self.num_pis:] = 1
+        self.net_slot = np.concatenate([np.arange(self.num_pis),
+                                        np.arange(self.num_gates)]).astype(np.int64)
+        return self
+
     @property
     def num_levels(self):
         return self.level_starts.size - 1
@@ -137,6 +159,12 @@ class Stimulus:
                 chunks.append(times[cuts[j]:cuts[j + 1]])
                 top += cuts[j + 1] - cuts[j]
         self.buf = np.concatenate(chunks).astype(np.int64) if chunks else np.zeros(0, np.int64)
+
+    @classmethod
+    def from_csr(cls, pi_off, pi_times, pi_init, boundaries):
+        waves = [(int(pi_init[p]), pi_times[pi_off[p]:pi_off[p + 1]])
+                 for p in range(len(pi_off) - 1)]
+        return cls(waves, boundaries)
 
     @property
     def num_windows(self):

@@ -84,13 +84,17 @@ struct gs_design {
   int device = 0;
   int P = 0, G = 0, N = 0, L = 0;
   std::vector<int64_t> level_starts;
-  std::vector<int> n_small;          // per level: gates with k <= 4 (ordered first)
+  // per level, gates grouped by fanin count: group g in 0..3 holds k = g+1,
+  // group 4 holds k > 4; grp[l*6 + g] .. grp[l*6 + g + 1] in device order
+  std::vector<int64_t> grp;
+  int64_t max_arc = 0, max_ic = 0;
   std::vector<int64_t> fanout;       // per net: input pins it drives
   std::vector<int> k_of;             // per gate
   int64_t sum_k = 0;
   int *order = nullptr, *gate_k = nullptr, *gate_pin = nullptr, *pin_net = nullptr,
       *pin_arc = nullptr;
   long long *pin_ic = nullptr, *arc = nullptr;
+  unsigned *arc32 = nullptr;
   unsigned long long *gate_lut = nullptr;
   unsigned *lut_words = nullptr;
 
@@ -108,11 +112,12 @@ struct gs_design {
     D.pin_ic = pin_ic;
     D.pin_arc = pin_arc;
     D.arc = arc;
+    D.arc32 = arc32;
     return D;
   }
   void release() {
     dfree(order); dfree(gate_k); dfree(gate_pin); dfree(pin_net); dfree(pin_arc);
-    dfree(pin_ic); dfree(arc); dfree(gate_lut); dfree(lut_words);
+    dfree(pin_ic); dfree(arc); dfree(arc32); dfree(gate_lut); dfree(lut_words);
   }
 };
 
@@ -161,28 +166,33 @@ static int design_build(const gs_design_desc *d, int device, gs_design *D) {
       if (n >= P && level_of[n - P] >= level_of[g])
         return fail(GS_ERR_ARG, "fanin is not on an earlier level");
       if (d->pin_ic[p] < 0) return fail(GS_ERR_ARG, "negative interconnect delay");
+      D->max_ic = std::max<int64_t>(D->max_ic, d->pin_ic[p]);
       if (d->pin_arc[p] < 0 || d->pin_arc[p] + (int64_t(1) << (k - 1)) > d->num_arc_rows)
         return fail(GS_ERR_ARG, "pin_arc out of range");
       D->fanout[n] += 1;
     }
   }
-  for (int64_t r = 0; r < 2 * d->num_arc_rows; ++r)
+  for (int64_t r = 0; r < 2 * d->num_arc_rows; ++r) {
     if (d->arc_rows[r] < 0) return fail(GS_ERR_ARG, "negative arc delay");
+    D->max_arc = std::max<int64_t>(D->max_arc, d->arc_rows[r]);
+  }
   D->sum_k = n_pins;
 
-  // ---- device order: per level, k <= 4 gates first (fast kernel), then k > 4
+  // ---- device order: per level, gates grouped k = 1, 2, 3, 4, then k > 4
+  // (one kernel instance per group keeps each hot loop small)
   std::vector<int> order(G);
-  D->n_small.assign(L, 0);
+  D->grp.assign((size_t)L * 6, 0);
   for (int64_t l = 0; l < L; ++l) {
     int64_t o = D->level_starts[l];
-    for (int pass = 0; pass < 2; ++pass)
+    for (int gi = 0; gi < 5; ++gi) {
+      D->grp[l * 6 + gi] = o;
       for (int64_t i = D->level_starts[l]; i < D->level_starts[l + 1]; ++i) {
         const int64_t g = d->order[i];
-        if ((D->k_of[g] <= 4) == (pass == 0)) {
-          order[o++] = (int)g;
-          if (pass == 0) D->n_small[l] += 1;
-        }
+        const int kg = std::min(D->k_of[g], 5) - 1;
+        if (kg == gi) order[o++] = (int)g;
       }
+    }
+    D->grp[l * 6 + 5] = o;
   }
   std::vector<int> gate_pin(G);
   std::vector<unsigned long long> gate_lut(G);
@@ -220,6 +230,11 @@ static int design_build(const gs_design_desc *d, int device, gs_design *D) {
   TRY(upload(&D->pin_arc, pin_arc.data(), n_pins));
   TRY(upload(&D->pin_ic, (const long long *)d->pin_ic, n_pins));
   TRY(upload(&D->arc, (const long long *)d->arc_rows, 2 * d->num_arc_rows));
+  if (D->max_arc < (int64_t(1) << 31) && D->max_ic < (int64_t(1) << 31)) {
+    std::vector<unsigned> a32(2 * d->num_arc_rows);
+    for (int64_t r = 0; r < 2 * d->num_arc_rows; ++r) a32[r] = (unsigned)d->arc_rows[r];
+    TRY(upload(&D->arc32, a32.data(), a32.size()));
+  }
   return GS_OK;
 }
 
@@ -231,6 +246,7 @@ struct gs_stim {
   int P = 0;
   int64_t W = 0;
   bool csr = true, wide = false;
+  int64_t max_wlen = 0;
   std::vector<int64_t> bnd_host;
   int64_t n_toggles = 0;
   long long *bnd = nullptr, *pi_off = nullptr, *pi_times = nullptr, *buf = nullptr,
@@ -272,6 +288,7 @@ static int stim_build(gs_design *D, const gs_stim_desc *s, gs_stim *S) {
     maxlen = std::max(maxlen, len);
   }
   S->wide = maxlen > (int64_t)0xFFFFFFFFll;
+  S->max_wlen = maxlen;
   S->csr = s->pi_off != nullptr;
   TRY(use_device(D->device));
   TRY(upload(&S->bnd, (const long long *)s->boundaries, S->W + 1));
@@ -331,6 +348,8 @@ struct gs_engine {
   int64_t pool_bytes = 0;            // requested gate-pool bytes
   int ncta_cap = 0;
   unsigned long long *bump = nullptr;
+  unsigned *work = nullptr;
+  int work_cap = 0;
   long long *acc = nullptr, *acc_run = nullptr;
   int *err = nullptr, *err_host = nullptr;
   unsigned long long *bump_host = nullptr;
@@ -355,6 +374,7 @@ struct gs_engine {
     dfree(a_buf);
     dfree(data);
     dfree(bump);
+    dfree(work);
     dfree(acc);
     dfree(acc_run);
     dfree(err);
@@ -371,14 +391,26 @@ struct gs_engine {
 
 namespace {
 
+template <typename K>
+int occupancy(K kernel, int *occ) {
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kernel, kEvalThreads, 0));
+  return GS_OK;
+}
+
+// persistent grid: the smallest occupancy of every kernel a run may launch
+// (all of them share the per-warp output regions, so one grid size)
 template <typename TS, int MODE>
-int grid_size(gs_engine *e, int *ncta) {
-  int a = 0, b = 0, c = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, gate_eval<TS, MODE, false>, kEvalThreads, 0));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, gate_eval<TS, MODE, true>, kEvalThreads, 0));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, stim_segment_win<TS>, kEvalThreads, 0));
-  int occ = std::max(1, std::min(a, std::min(b, c)));
-  *ncta = e->sms * occ;
+int grid_size(gs_engine *e, bool narrow, int *ncta) {
+  int occ = 1 << 20, o = 0;
+  if (narrow) {
+    TRY(occupancy(gate_eval<TS, unsigned, MODE, 1>, &o)); occ = std::min(occ, o);
+    TRY(occupancy(gate_eval<TS, unsigned, MODE, 2>, &o)); occ = std::min(occ, o);
+    TRY(occupancy(gate_eval<TS, unsigned, MODE, 3>, &o)); occ = std::min(occ, o);
+    TRY(occupancy(gate_eval<TS, unsigned, MODE, 4>, &o)); occ = std::min(occ, o);
+  }
+  TRY(occupancy(gate_eval<TS, long long, MODE, 0>, &o)); occ = std::min(occ, o);
+  TRY(occupancy(stim_segment_win<TS>, &o)); occ = std::min(occ, o);
+  *ncta = e->sms * std::max(1, occ);
   return GS_OK;
 }
 
@@ -438,15 +470,25 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
   const int64_t N = D->N, G = D->G;
   const bool arena = MODE != MODE_STATS;
   const bool store = MODE == MODE_STORE;
+  // 32-bit time arithmetic when every sum the event loop forms stays below
+  // 2^32-1: relative time < window length, plus interconnect, plus arc delay
+  const bool narrow = sizeof(TS) == 4 && D->arc32 != nullptr &&
+                      s->max_wlen + D->max_ic + D->max_arc <= (int64_t)0xFFFFFFFEll;
   int ncta = 0;
-  TRY((grid_size<TS, MODE>(e, &ncta)));
-  if (ncta > e->ncta_cap) {
+  TRY((grid_size<TS, MODE>(e, narrow, &ncta)));
+  const int nregions = ncta * kEvalWarps;
+  if (nregions > e->ncta_cap) {
     dfree(e->bump);
     if (e->bump_host) cudaFreeHost(e->bump_host);
     e->bump_host = nullptr;
-    TRY(dalloc(&e->bump, ncta));
-    CK(cudaMallocHost((void **)&e->bump_host, sizeof(unsigned long long) * ncta));
-    e->ncta_cap = ncta;
+    TRY(dalloc(&e->bump, nregions));
+    CK(cudaMallocHost((void **)&e->bump_host, sizeof(unsigned long long) * nregions));
+    e->ncta_cap = nregions;
+  }
+  if (e->work_cap < D->L * 5 + 1) {
+    dfree(e->work);
+    TRY(dalloc(&e->work, (size_t)D->L * 5 + 1));
+    e->work_cap = D->L * 5 + 1;
   }
   const int64_t per_win = meta_bytes_per_window(D, arena);
   const int64_t pi_words = s->csr ? s->n_toggles : 0;
@@ -483,7 +525,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     // gate pool: generous estimate of stored toggles, at least 64 MiB
     const int64_t meta_now = per_win * Wpad;
     int64_t room = e->budget - meta_now - pi_bytes;
-    if (room < (int64_t)ncta * 4096) {
+    if (room < (int64_t)nregions * 4096) {
       if (Wc > kWarp) { Wc = std::max<int64_t>(kWarp, Wc / 2 / kWarp * kWarp); continue; }
       return fail(GS_ERR_CAPACITY, "device memory budget cannot hold one 32-window chunk");
     }
@@ -493,7 +535,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     want = std::min(want, room);
     TRY(ensure_data(e, pi_bytes + want));
     const int64_t pool_words = (e->data_bytes - pi_bytes) / (int64_t)sizeof(TS);
-    const int64_t part_words = pool_words / ncta;
+    const int64_t part_words = pool_words / nregions;
 
     ChunkDev C;
     memset(&C, 0, sizeof(C));
@@ -510,6 +552,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     C.pool_base = (unsigned long long)(pi_bytes / (int64_t)sizeof(TS));
     C.part_words = (unsigned long long)part_words;
     C.bump = e->bump;
+    C.work = e->work;
     C.acc = e->acc;
     C.err = e->err;
     if (arena) {
@@ -528,7 +571,8 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
       }
     }
     CK(cudaMemsetAsync(e->acc, 0, sizeof(long long) * ACC_ROWS * N, e->st));
-    CK(cudaMemsetAsync(e->bump, 0, sizeof(unsigned long long) * ncta, e->st));
+    CK(cudaMemsetAsync(e->bump, 0, sizeof(unsigned long long) * nregions, e->st));
+    CK(cudaMemsetAsync(e->work, 0, sizeof(unsigned) * (D->L * 5 + 1), e->st));
     CK(cudaMemsetAsync(e->err, 0, sizeof(int) * ERR_NFLAGS, e->st));
     CK(cudaEventRecord(e->ev[0], e->st));
     // ---- K1
@@ -547,34 +591,42 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
       k1 = 1;
     }
     CK(cudaEventRecord(e->ev[1], e->st));
-    // ---- K4, one launch per level (kernel boundary = level barrier)
-    const int64_t warps = (int64_t)ncta * kEvalWarps;
+    // ---- K4: per level, one launch per fanin-count group (the launch
+    // boundary between levels is the level barrier)
+    const int64_t warps = (int64_t)nregions;
     int nl = 0;
     for (int l = 0; l < D->L; ++l) {
-      const int lo = (int)D->level_starts[l];
-      const int n_all = (int)(D->level_starts[l + 1] - D->level_starts[l]);
-      const int n_small = D->n_small[l];
-      for (int part = 0; part < 2; ++part) {
-        const int n = part == 0 ? n_small : n_all - n_small;
+      for (int gi = 0; gi < 5; ++gi) {
+        const int lo = (int)D->grp[l * 6 + gi];
+        const int n = (int)(D->grp[l * 6 + gi + 1] - lo);
         if (n <= 0) continue;
         LevelArgs A;
-        A.lo = part == 0 ? lo : lo + n_small;
+        A.lo = lo;
         A.n = n;
-        A.tpi = (int)std::max<int64_t>(1, std::min<int64_t>(32, (int64_t)n * Tc / (8 * warps)));
+        // items of tpi tiles: enough items for dynamic balance, few enough
+        // that per-item setup and work-counter atomics stay negligible
+        A.tpi = (int)std::max<int64_t>(1, std::min<int64_t>(16, (int64_t)n * Tc / (16 * warps)));
         A.tpi = std::min(A.tpi, Tc);
         A.ntg = (Tc + A.tpi - 1) / A.tpi;
         A.pct = pct;
-        if (part == 0)
-          gate_eval<TS, MODE, false><<<ncta, kEvalThreads, 0, e->st>>>(Dd, C, A);
+        A.counter = l * 5 + gi;
+        if (narrow && gi == 0)
+          gate_eval<TS, unsigned, MODE, 1><<<ncta, kEvalThreads, 0, e->st>>>(Dd, C, A);
+        else if (narrow && gi == 1)
+          gate_eval<TS, unsigned, MODE, 2><<<ncta, kEvalThreads, 0, e->st>>>(Dd, C, A);
+        else if (narrow && gi == 2)
+          gate_eval<TS, unsigned, MODE, 3><<<ncta, kEvalThreads, 0, e->st>>>(Dd, C, A);
+        else if (narrow && gi == 3)
+          gate_eval<TS, unsigned, MODE, 4><<<ncta, kEvalThreads, 0, e->st>>>(Dd, C, A);
         else
-          gate_eval<TS, MODE, true><<<ncta, kEvalThreads, 0, e->st>>>(Dd, C, A);
+          gate_eval<TS, long long, MODE, 0><<<ncta, kEvalThreads, 0, e->st>>>(Dd, C, A);
         CK(cudaGetLastError());
         ++nl;
       }
     }
     CK(cudaEventRecord(e->ev[2], e->st));
     CK(cudaMemcpyAsync(e->err_host, e->err, sizeof(int) * ERR_NFLAGS, cudaMemcpyDeviceToHost, e->st));
-    CK(cudaMemcpyAsync(e->bump_host, e->bump, sizeof(unsigned long long) * ncta,
+    CK(cudaMemcpyAsync(e->bump_host, e->bump, sizeof(unsigned long long) * nregions,
                        cudaMemcpyDeviceToHost, e->st));
     CK(cudaStreamSynchronize(e->st));
     if (e->err_host[ERR_CAP])
@@ -592,8 +644,8 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
       continue;
     }
     unsigned long long used = 0;
-    for (int c = 0; c < ncta; ++c) used = std::max(used, e->bump_host[c]);
-    peak_bytes = std::max<int64_t>(peak_bytes, (int64_t)(used * ncta * sizeof(TS)) + pi_bytes);
+    for (int c = 0; c < nregions; ++c) used = std::max(used, e->bump_host[c]);
+    peak_bytes = std::max<int64_t>(peak_bytes, (int64_t)(used * nregions * sizeof(TS)) + pi_bytes);
     float a = 0.f, b = 0.f;
     CK(cudaEventElapsedTime(&a, e->ev[0], e->ev[1]));
     CK(cudaEventElapsedTime(&b, e->ev[1], e->ev[2]));

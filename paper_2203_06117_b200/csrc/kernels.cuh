@@ -55,6 +55,7 @@ struct DesignDev {
   const long long *pin_ic;     // [sum k]
   const int *pin_arc;          // [sum k] first condition row of the pin
   const long long *arc;        // [R*2] (rise, fall)
+  const unsigned *arc32;       // same, 32-bit (narrow kernels; null if delays >= 2^31)
 };
 
 struct ChunkDev {
@@ -65,8 +66,9 @@ struct ChunkDev {
   unsigned long long *tbase;
   unsigned *init;
   void *data;                  // TS[]
-  unsigned long long pool_base, part_words;  // per-CTA regions of `data`
-  unsigned long long *bump;    // [gridDim.x] words used in each region
+  unsigned long long pool_base, part_words;  // per-warp regions of `data`
+  unsigned long long *bump;    // [gridDim.x * kEvalWarps] words used in each region
+  unsigned *work;              // per-launch work counters (dynamic item fetch)
   long long *acc;              // [ACC_ROWS][N]
   int *err;                    // [ERR_NFLAGS]
   // arena mode ([G][Wpad] by gate id)
@@ -93,6 +95,7 @@ struct LevelArgs {
   int lo, n;                   // gates order[lo, lo+n)
   int tpi, ntg;                // tiles per item, tile groups per gate
   int pct;
+  int counter;                 // index into ChunkDev::work
 };
 
 // ---------------------------------------------------------------- helpers
@@ -135,16 +138,20 @@ __device__ __forceinline__ long long lower_bound(const long long *__restrict__ a
   return lo;
 }
 
-// bump-allocate `words` in this CTA's region; returns absolute index or ~0ull
+// bump-allocate `words` (warp-uniform) in this warp's private region of the
+// pool; returns the absolute index in `data` (same on all lanes) or ~0ull when
+// the region is full (the chunk is then re-run with more room)
 __device__ __forceinline__ unsigned long long region_alloc(const ChunkDev &C,
-                                                           unsigned long long *s_bump,
+                                                           unsigned long long &bump,
+                                                           unsigned long long region,
                                                            unsigned long long words) {
-  unsigned long long old = atomicAdd(s_bump, words);
+  const unsigned long long old = bump;
   if (old + words > C.part_words) {
-    atomicExch(C.err + ERR_POOL, 1);
+    if (lane_id() == 0) atomicExch(C.err + ERR_POOL, 1);
     return ~0ull;
   }
-  return C.pool_base + (unsigned long long)blockIdx.x * C.part_words + old;
+  bump = old + words;
+  return C.pool_base + region * C.part_words + old;
 }
 
 // warp-wide sum of five per-lane partials, added by lane 0 into acc[row][net]
@@ -235,11 +242,10 @@ __global__ void __launch_bounds__(256) stim_segment_csr(StimDev S, ChunkDev C, i
 template <typename TS>
 __global__ void __launch_bounds__(kEvalThreads) stim_segment_win(StimDev S, ChunkDev C, int tpi,
                                                                  int ntg) {
-  __shared__ unsigned long long s_bump;
-  if (threadIdx.x == 0) s_bump = C.bump[blockIdx.x];
-  __syncthreads();
   const unsigned lane = lane_id();
   const int warp = threadIdx.x / kWarp;
+  const unsigned long long region = (unsigned long long)blockIdx.x * kEvalWarps + warp;
+  unsigned long long bump = C.bump[region];
   const long long items = (long long)S.P * ntg;
   TS *data = reinterpret_cast<TS *>(C.data);
   for (long long it = blockIdx.x + (long long)gridDim.x * warp; it < items;
@@ -264,9 +270,7 @@ __global__ void __launch_bounds__(kEvalThreads) stim_segment_win(StimDev S, Chun
       }
       unsigned total;
       const unsigned ex = warp_excl_scan(c, &total);
-      unsigned long long base = 0;
-      if (lane == 0) base = total ? region_alloc(C, &s_bump, total) : 0ull;
-      base = __shfl_sync(0xffffffffu, base, 0);
+      const unsigned long long base = total ? region_alloc(C, bump, region, total) : 0ull;
       const unsigned word = __ballot_sync(0xffffffffu, v0);
       const bool wrote = base != ~0ull;
       if (lane == 0) {
@@ -291,34 +295,61 @@ __global__ void __launch_bounds__(kEvalThreads) stim_segment_win(StimDev S, Chun
     }
     acc_flush(C, p, t1, tc, 0, 0, 0);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) C.bump[blockIdx.x] = s_bump;
+  if (lane == 0) C.bump[region] = bump;
 }
 
 // ------------------------------------------------------------------- K4
 // Algo. 1 for one gate over one 32-window tile; lane = window.
-// K > 0: fanin count known at compile time (fully unrolled, registers);
-// K == 0: generic k <= 16 (separate kernel, so its register footprint does not
-// cap the occupancy of the common k <= 4 kernel).
-template <typename TS, int MODE, int K>
+//   K > 0 : fanin count fixed at compile time (fully unrolled, registers);
+//   K == 0: generic k <= 16 (runtime loops).
+//   TT    : time arithmetic -- unsigned (narrow: every window length plus the
+//           largest interconnect and arc delay fits below 2^32-1) or long long.
+// One kernel instance per (K, TT) keeps each hot loop small enough for the
+// instruction cache; gates of a level are grouped by k on the host.
+template <typename TT>
+struct TimeTraits;
+template <>
+struct TimeTraits<unsigned> {
+  static __device__ __forceinline__ unsigned inf() { return 0xffffffffu; }
+};
+template <>
+struct TimeTraits<long long> {
+  static __device__ __forceinline__ long long inf() { return kInf; }
+};
+
+template <typename TT>
+__device__ __forceinline__ TT arc_delay(const DesignDev &D, int row, int col);
+template <>
+__device__ __forceinline__ unsigned arc_delay<unsigned>(const DesignDev &D, int row, int col) {
+  return __ldg(D.arc32 + (size_t)row * 2 + col);
+}
+template <>
+__device__ __forceinline__ long long arc_delay<long long>(const DesignDev &D, int row, int col) {
+  return __ldg(D.arc + (size_t)row * 2 + col);
+}
+
+template <typename TS, typename TT, int MODE, int K>
 __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C, int g, int k,
                                           unsigned long long lut, const int *net,
-                                          const long long *ic, const int *arc, int t, int pct,
-                                          TS *slab, unsigned long long *s_bump, long long &acc_t1,
+                                          const TT *ic, const int *arc, int t, int pct,
+                                          TS *slab, unsigned long long &bump,
+                                          unsigned long long region, long long &acc_t1,
                                           long long &acc_tc, long long &acc_filt,
                                           long long &acc_icf, long long &acc_disc) {
   constexpr int KM = K > 0 ? K : kMaxK;
   const int kk = K > 0 ? K : k;
+  const TT INF = TimeTraits<TT>::inf();
   const unsigned lane = lane_id();
   const int wr = t * kWarp + (int)lane;
   const bool act = wr < C.Wc;
   const long long wabs = C.w0 + wr;
   TS *data = reinterpret_cast<TS *>(C.data);
-  long long b_lo = 0, wlen = 0;
+  long long b_lo = 0, wlen64 = 0;
   if (act) {
     b_lo = C.bnd[wabs];
-    wlen = C.bnd[wabs + 1] - b_lo;
+    wlen64 = C.bnd[wabs + 1] - b_lo;
   }
+  const TT wlen = (TT)wlen64;
 
   // fanin tiles: counts, bases, window-start bits (init_values + level_ub fused)
   const TS *sp[KM];
@@ -339,7 +370,7 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   }
   const unsigned y0 = act ? lut_bit(lut, kk, D.lut_words, idx) : 0u;
 
-  // output staging: smem slab when the tile's bound fits, else the CTA region
+  // output staging: smem slab when the tile's bound fits, else this warp's region
   unsigned UB;
   const unsigned ubx = warp_excl_scan(ub, &UB);
   TS *st;
@@ -347,45 +378,43 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   if (UB <= (unsigned)kSlab) {
     st = slab + ubx;
   } else {
-    unsigned long long sb = 0;
-    if (lane == 0) sb = region_alloc(C, s_bump, UB);
-    sb = __shfl_sync(0xffffffffu, sb, 0);
+    const unsigned long long sb = region_alloc(C, bump, region, UB);
     ok = sb != ~0ull;
     st = data + (ok ? sb : 0ull) + ubx;
   }
 
   // ---- per-lane event loop (sim_span, _kernels.py:94-203)
   unsigned pos[KM];
-  long long nxt[KM];
+  TT nxt[KM];
 #pragma unroll
-  for (int p = 0; p < kk; ++p) { pos[p] = 0; nxt[p] = kInf; }
+  for (int p = 0; p < kk; ++p) { pos[p] = 0; nxt[p] = INF; }
   unsigned need = (act && ok) ? ((1u << kk) - 1u) : 0u;
   unsigned y = y0;
   int cnt = 0, peak = 0, filt = 0, icf = 0, disc = 0;
   bool has_last = false, last_stored = false;
-  long long t_last = 0;
+  TT t_last = 0;
   const int cap = (int)ub;  // peak <= #events <= sum of fanin toggles
   while (true) {
-    long long tmin = kInf;
+    TT tmin = INF;
 #pragma unroll
     for (int p = 0; p < kk; ++p) {
       if ((need >> p) & 1u) {
         // interconnect inertial filter: drop adjacent pairs narrower than d
-        const long long d = ic[p];
+        const TT d = ic[p];
         unsigned q = pos[p];
         const TS *s = sp[p];
         if (d > 0) {
-          while (q + 1 < n[p] && (long long)__ldg(s + q + 1) - (long long)__ldg(s + q) < d) {
+          while (q + 1 < n[p] && (TT)__ldg(s + q + 1) - (TT)__ldg(s + q) < d) {
             q += 2;
             ++icf;
           }
         }
         pos[p] = q;
-        nxt[p] = q < n[p] ? (long long)__ldg(s + q) + d : kInf;
+        nxt[p] = q < n[p] ? (TT)__ldg(s + q) + d : INF;
       }
       tmin = min(tmin, nxt[p]);
     }
-    if (tmin == kInf) break;
+    if (tmin == INF) break;
     // multiple simultaneous inputs: consume every pin arriving at tmin
     unsigned sw = 0;
 #pragma unroll
@@ -401,18 +430,18 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
     if (ny != y) {
       // conditional SDF: max over switching arcs, rows from the post state
       const int col = ny ? 0 : 1;
-      long long dly = 0;
+      TT dly = 0;
 #pragma unroll
       for (int p = 0; p < kk; ++p) {
         if ((sw >> p) & 1u) {
-          const unsigned row = (idx & ((1u << p) - 1u)) | ((idx >> (p + 1)) << p);
-          dly = max(dly, __ldg(D.arc + ((long long)arc[p] + row) * 2 + col));
+          const int row = (int)((idx & ((1u << p) - 1u)) | ((idx >> (p + 1)) << p));
+          dly = max(dly, arc_delay<TT>(D, arc[p] + row, col));
         }
       }
-      const long long t_out = tmin + dly;
-      const long long thr = dly * pct / 100;
+      const TT t_out = tmin + dly;
+      const TT thr = (TT)((unsigned long long)dly * (unsigned)pct / 100u);
       const bool have = has_last || cnt > 0;
-      const long long tgt = has_last ? t_last : (cnt > 0 ? (long long)st[cnt - 1] : 0);
+      const TT tgt = has_last ? t_last : (cnt > 0 ? (TT)st[cnt - 1] : (TT)0);
       if (have && (t_out <= tgt || t_out - tgt < thr)) {
         // inertial rejection: the pulse is cancelled in full
         if (has_last) {
@@ -445,31 +474,13 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
     ++cnt;
     peak = max(peak, cnt);
   }
+  if (!(act && ok)) cnt = peak = 0;
 
-  // ---- fused dwell / toggle reduction (dwell_sweep, gate rows)
-  if (act && ok) {
-    unsigned v = y0;
-    long long prev = 0, t1 = 0;
-    for (int j = 0; j < cnt; ++j) {
-      const long long x = (long long)st[j];
-      if (v) t1 += x - prev;
-      v ^= 1u;
-      prev = x;
-    }
-    if (v) t1 += wlen - prev;
-    acc_t1 += t1;
-    acc_tc += cnt;
-    acc_filt += filt;
-    acc_icf += icf;
-    acc_disc += disc;
-  }
-
-  // ---- compaction: warp scan of counts, one region allocation per tile
+  // ---- compaction: warp scan of counts, one region allocation per tile;
+  // the copy out of the staging area also yields the dwell at 1 (dwell_sweep)
   unsigned CNT;
   const unsigned cx = warp_excl_scan((unsigned)cnt, &CNT);
-  unsigned long long ob = 0;
-  if (lane == 0) ob = CNT ? region_alloc(C, s_bump, CNT) : 0ull;
-  ob = __shfl_sync(0xffffffffu, ob, 0);
+  const unsigned long long ob = CNT ? region_alloc(C, bump, region, CNT) : 0ull;
   const bool wrote = ob != ~0ull;  // else the chunk is re-run; keep readers in bounds
   const unsigned word = __ballot_sync(0xffffffffu, y0);
   const int gnet = D.P + g;
@@ -479,10 +490,22 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   }
   if (act) {
     C.cnt[(size_t)gnet * C.Wpad + wr] = wrote ? (unsigned)cnt : 0u;
-    if (wrote) {
-      TS *dst = data + ob + cx;
-      for (int j = 0; j < cnt; ++j) dst[j] = st[j];
+    TS *dst = data + (wrote ? ob + cx : 0ull);
+    unsigned v = y0;
+    long long prev = 0, t1 = 0;
+    for (int j = 0; j < cnt; ++j) {
+      const TS x = st[j];
+      if (wrote) dst[j] = x;
+      if (v) t1 += (long long)x - prev;
+      v ^= 1u;
+      prev = (long long)x;
     }
+    if (v) t1 += wlen64 - prev;
+    acc_t1 += t1;
+    acc_tc += cnt;
+    acc_filt += filt;
+    acc_icf += icf;
+    acc_disc += disc;
     if (MODE & MODE_COUNTERS) {
       const size_t gw = (size_t)g * C.Wpad + wr;
       C.a_cnt[gw] = cnt;
@@ -506,63 +529,48 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   __syncwarp();
 }
 
-template <typename TS, int MODE, int K>
-__device__ __forceinline__ void eval_item(const DesignDev &D, const ChunkDev &C, int g, int k,
-                                          int pin0, unsigned long long lut, int t_lo, int t_hi,
-                                          int pct, TS *slab, unsigned long long *s_bump) {
-  constexpr int KM = K > 0 ? K : kMaxK;
-  const int kk = K > 0 ? K : k;
-  int net[KM], arc[KM];
-  long long ic[KM];
-#pragma unroll
-  for (int p = 0; p < kk; ++p) {
-    net[p] = __ldg(D.pin_net + pin0 + p);
-    ic[p] = __ldg(D.pin_ic + pin0 + p);
-    arc[p] = __ldg(D.pin_arc + pin0 + p);
-  }
-  long long t1 = 0, tc = 0, filt = 0, icf = 0, disc = 0;
-  for (int t = t_lo; t < t_hi; ++t)
-    eval_tile<TS, MODE, K>(D, C, g, kk, lut, net, ic, arc, t, pct, slab, s_bump, t1, tc, filt,
-                           icf, disc);
-  acc_flush(C, D.P + g, t1, tc, filt, icf, disc);
-}
-
-// One launch per logic level (the level barrier is the launch boundary).
-// Persistent grid; item i = (gate i / ntg, tile group i % ntg) goes to CTA
-// i % gridDim.x, so every CTA's output region fills evenly.  GENERIC selects
-// the k > 4 instantiation (gates of a level are ordered k <= 4 first).
-template <typename TS, int MODE, bool GENERIC>
+// One launch per (logic level, fanin-count group); the level barrier is the
+// launch boundary.  Persistent grid with dynamic work fetching: each warp takes
+// the next item (gate, group of tpi tiles) from a per-launch counter, and owns
+// a private output region (no CTA barrier, no global atomics on the data path).
+template <typename TS, typename TT, int MODE, int K>
 __global__ void __launch_bounds__(kEvalThreads) gate_eval(DesignDev D, ChunkDev C, LevelArgs A) {
+  constexpr int KM = K > 0 ? K : kMaxK;
   __shared__ TS s_slab[kEvalWarps][kSlab];
-  __shared__ unsigned long long s_bump;
-  if (threadIdx.x == 0) s_bump = C.bump[blockIdx.x];
-  __syncthreads();
   const int warp = threadIdx.x / kWarp;
+  const unsigned lane = lane_id();
+  const unsigned long long region = (unsigned long long)blockIdx.x * kEvalWarps + warp;
+  unsigned long long bump = C.bump[region];
   const long long items = (long long)A.n * A.ntg;
-  for (long long it = blockIdx.x + (long long)gridDim.x * warp; it < items;
-       it += (long long)gridDim.x * kEvalWarps) {
+  TS *slab = s_slab[warp];
+  while (true) {
+    long long it = 0;
+    if (lane == 0) it = (long long)atomicAdd(C.work + A.counter, 1u);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= items) break;
     const int j = (int)(it / A.ntg);
     const int tg = (int)(it % A.ntg);
     const int g = __ldg(D.order + A.lo + j);
-    const int k = __ldg(D.gate_k + g);
+    const int k = K > 0 ? K : __ldg(D.gate_k + g);
     const int pin0 = __ldg(D.gate_pin + g);
     const unsigned long long lut = __ldg(D.gate_lut + g);
     const int t_lo = tg * A.tpi;
     const int t_hi = min(t_lo + A.tpi, C.Tc);
-    TS *slab = s_slab[warp];
-    if (GENERIC) {
-      eval_item<TS, MODE, 0>(D, C, g, k, pin0, lut, t_lo, t_hi, A.pct, slab, &s_bump);
-    } else {
-      switch (k) {
-        case 1: eval_item<TS, MODE, 1>(D, C, g, 1, pin0, lut, t_lo, t_hi, A.pct, slab, &s_bump); break;
-        case 2: eval_item<TS, MODE, 2>(D, C, g, 2, pin0, lut, t_lo, t_hi, A.pct, slab, &s_bump); break;
-        case 3: eval_item<TS, MODE, 3>(D, C, g, 3, pin0, lut, t_lo, t_hi, A.pct, slab, &s_bump); break;
-        default: eval_item<TS, MODE, 4>(D, C, g, 4, pin0, lut, t_lo, t_hi, A.pct, slab, &s_bump); break;
-      }
+    int net[KM], arc[KM];
+    TT ic[KM];
+#pragma unroll
+    for (int p = 0; p < (K > 0 ? K : k); ++p) {
+      net[p] = __ldg(D.pin_net + pin0 + p);
+      ic[p] = (TT)__ldg(D.pin_ic + pin0 + p);
+      arc[p] = __ldg(D.pin_arc + pin0 + p);
     }
+    long long t1 = 0, tc = 0, filt = 0, icf = 0, disc = 0;
+    for (int t = t_lo; t < t_hi; ++t)
+      eval_tile<TS, TT, MODE, K>(D, C, g, k, lut, net, ic, arc, t, A.pct, slab, bump, region,
+                                 t1, tc, filt, icf, disc);
+    acc_flush(C, D.P + g, t1, tc, filt, icf, disc);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) C.bump[blockIdx.x] = s_bump;
+  if (lane == 0) C.bump[region] = bump;
 }
 
 // chunk accumulators -> run accumulators [t1 | tc | ig | filtered, icf, disc]
