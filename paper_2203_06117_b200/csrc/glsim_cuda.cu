@@ -391,26 +391,57 @@ struct gs_engine {
 
 namespace {
 
-template <typename K>
-int occupancy(K kernel, int *occ) {
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kernel, kEvalThreads, 0));
+// Per gate_eval instantiation: opt in to its dynamic shared memory (per-warp
+// tile state, above the 48 KB static limit) and size its persistent grid from
+// its own occupancy.  Output regions are indexed by (CTA, warp), so every
+// launch of a chunk shares the region array sized by the largest grid.
+template <typename TS, typename TT, int MODE, int K, bool P100>
+int eval_grid(int sms, int *grid) {
+  static int cached = 0;
+  if (!cached) {
+    const size_t smem = eval_smem_bytes<TS, TT, K>();
+    CK(cudaFuncSetAttribute(gate_eval<TS, TT, MODE, K, P100>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gate_eval<TS, TT, MODE, K, P100>,
+                                                     kEvalThreads, smem));
+    cached = std::max(1, occ);
+  }
+  *grid = sms * cached;
   return GS_OK;
 }
 
-// persistent grid: the smallest occupancy of every kernel a run may launch
-// (all of them share the per-warp output regions, so one grid size)
+template <typename TS, typename TT, int MODE, int K, bool P100>
+int launch_eval(int sms, cudaStream_t st, const DesignDev &Dd, const ChunkDev &C,
+                const LevelArgs &A, int max_grid) {
+  int grid = 0;
+  TRY((eval_grid<TS, TT, MODE, K, P100>(sms, &grid)));
+  grid = std::min(grid, max_grid);
+  gate_eval<TS, TT, MODE, K, P100><<<grid, kEvalThreads, eval_smem_bytes<TS, TT, K>(), st>>>(Dd, C, A);
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
+// largest persistent grid any kernel of a run may use (sizes the regions)
 template <typename TS, int MODE>
-int grid_size(gs_engine *e, bool narrow, int *ncta) {
-  int occ = 1 << 20, o = 0;
-  if (narrow) {
-    TRY(occupancy(gate_eval<TS, unsigned, MODE, 1>, &o)); occ = std::min(occ, o);
-    TRY(occupancy(gate_eval<TS, unsigned, MODE, 2>, &o)); occ = std::min(occ, o);
-    TRY(occupancy(gate_eval<TS, unsigned, MODE, 3>, &o)); occ = std::min(occ, o);
-    TRY(occupancy(gate_eval<TS, unsigned, MODE, 4>, &o)); occ = std::min(occ, o);
+int grid_size(gs_engine *e, bool narrow, bool p100, int *ncta) {
+  int g = 0, best = 0;
+  if (narrow && p100) {
+    TRY((eval_grid<TS, unsigned, MODE, 1, true>(e->sms, &g))); best = std::max(best, g);
+    TRY((eval_grid<TS, unsigned, MODE, 2, true>(e->sms, &g))); best = std::max(best, g);
+    TRY((eval_grid<TS, unsigned, MODE, 3, true>(e->sms, &g))); best = std::max(best, g);
+    TRY((eval_grid<TS, unsigned, MODE, 4, true>(e->sms, &g))); best = std::max(best, g);
+  } else if (narrow) {
+    TRY((eval_grid<TS, unsigned, MODE, 1, false>(e->sms, &g))); best = std::max(best, g);
+    TRY((eval_grid<TS, unsigned, MODE, 2, false>(e->sms, &g))); best = std::max(best, g);
+    TRY((eval_grid<TS, unsigned, MODE, 3, false>(e->sms, &g))); best = std::max(best, g);
+    TRY((eval_grid<TS, unsigned, MODE, 4, false>(e->sms, &g))); best = std::max(best, g);
   }
-  TRY(occupancy(gate_eval<TS, long long, MODE, 0>, &o)); occ = std::min(occ, o);
-  TRY(occupancy(stim_segment_win<TS>, &o)); occ = std::min(occ, o);
-  *ncta = e->sms * std::max(1, occ);
+  TRY((eval_grid<TS, long long, MODE, 0, false>(e->sms, &g))); best = std::max(best, g);
+  int o = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, stim_segment_win<TS>, kEvalThreads, 0));
+  best = std::max(best, e->sms * std::max(1, o));
+  *ncta = best;
   return GS_OK;
 }
 
@@ -419,10 +450,10 @@ int ensure_meta(gs_engine *e, int64_t wins) {
   if (e->meta_windows >= wins) return GS_OK;
   e->release_meta();
   const int64_t N = e->d->N;
-  const int64_t Wpad = round_up(wins, kWarp);
+  const int64_t Wpad = round_up(wins, kTile);
   TRY(dalloc(&e->cnt, (size_t)(N * Wpad)));
-  TRY(dalloc(&e->tbase, (size_t)(N * (Wpad / kWarp))));
-  TRY(dalloc(&e->init, (size_t)(N * (Wpad / kWarp))));
+  TRY(dalloc(&e->tbase, (size_t)(N * (Wpad / kTile))));
+  TRY(dalloc(&e->init, (size_t)(N * (Wpad / 32))));
   e->meta_windows = Wpad;
   return GS_OK;
 }
@@ -430,7 +461,7 @@ int ensure_meta(gs_engine *e, int64_t wins) {
 int ensure_arena(gs_engine *e, int64_t wins, bool store) {
   if (e->arena_windows >= wins && (!store || e->a_off)) return GS_OK;
   e->release_arena();
-  const size_t n = (size_t)e->d->G * (size_t)round_up(wins, kWarp);
+  const size_t n = (size_t)e->d->G * (size_t)round_up(wins, kTile);
   TRY(dalloc(&e->a_cnt, n));
   TRY(dalloc(&e->a_peak, n));
   TRY(dalloc(&e->a_filt, n));
@@ -438,7 +469,7 @@ int ensure_arena(gs_engine *e, int64_t wins, bool store) {
   TRY(dalloc(&e->a_disc, n));
   TRY(dalloc(&e->a_init, n));
   TRY(dalloc(&e->a_off, n));
-  e->arena_windows = round_up(wins, kWarp);
+  e->arena_windows = round_up(wins, kTile);
   return GS_OK;
 }
 
@@ -452,7 +483,7 @@ int ensure_data(gs_engine *e, int64_t bytes) {
 }
 
 int64_t meta_bytes_per_window(const gs_design *d, bool arena) {
-  int64_t b = (int64_t)d->N * 4 + (int64_t)d->N * 12 / kWarp + 1;
+  int64_t b = (int64_t)d->N * 4 + (int64_t)d->N * (8 / kTile + 4 / 32) + d->N / 8 + 1;
   if (arena) b += (int64_t)d->G * (6 * 8 + 1);
   return b;
 }
@@ -474,8 +505,9 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
   // 2^32-1: relative time < window length, plus interconnect, plus arc delay
   const bool narrow = sizeof(TS) == 4 && D->arc32 != nullptr &&
                       s->max_wlen + D->max_ic + D->max_arc <= (int64_t)0xFFFFFFFEll;
+  const bool p100 = pct == 100;
   int ncta = 0;
-  TRY((grid_size<TS, MODE>(e, narrow, &ncta)));
+  TRY((grid_size<TS, MODE>(e, narrow, p100, &ncta)));
   const int nregions = ncta * kEvalWarps;
   if (nregions > e->ncta_cap) {
     dfree(e->bump);
@@ -496,9 +528,9 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
   const int64_t total = w_hi - w_lo;
   // initial chunk: metadata takes at most ~40% of the budget
   int64_t Wc = e->chunk_hint > 0 ? e->chunk_hint
-                                  : std::max<int64_t>(kWarp, (e->budget * 2 / 5) / per_win);
-  Wc = std::min<int64_t>(Wc, round_up(total, kWarp));
-  Wc = std::max<int64_t>(kWarp, Wc / kWarp * kWarp);
+                                  : std::max<int64_t>(kTile, (e->budget * 2 / 5) / per_win);
+  Wc = std::min<int64_t>(Wc, round_up(total, kTile));
+  Wc = std::max<int64_t>(kTile, Wc / kTile * kTile);
   const double density = (s->P && s->W) ? (double)s->n_toggles / ((double)s->P * s->W) : 0.0;
 
   if (store) {
@@ -518,16 +550,16 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
   int64_t pool_bytes = e->pool_bytes;
   while (w < w_hi) {
     const int64_t wc = std::min<int64_t>(Wc, w_hi - w);
-    const int64_t Wpad = round_up(wc, kWarp);
-    const int Tc = (int)(Wpad / kWarp);
+    const int64_t Wpad = round_up(wc, kTile);
+    const int Tc = (int)(Wpad / kTile);
     TRY(ensure_meta(e, Wpad));
     if (arena) TRY(ensure_arena(e, Wpad, store));
     // gate pool: generous estimate of stored toggles, at least 64 MiB
     const int64_t meta_now = per_win * Wpad;
     int64_t room = e->budget - meta_now - pi_bytes;
     if (room < (int64_t)nregions * 4096) {
-      if (Wc > kWarp) { Wc = std::max<int64_t>(kWarp, Wc / 2 / kWarp * kWarp); continue; }
-      return fail(GS_ERR_CAPACITY, "device memory budget cannot hold one 32-window chunk");
+      if (Wc > kTile) { Wc = std::max<int64_t>(kTile, Wc / 2 / kTile * kTile); continue; }
+      return fail(GS_ERR_CAPACITY, "device memory budget cannot hold one 128-window chunk");
     }
     const double est_words = (double)G * wc * std::max(2.0, 4.0 * density) * 2.0;
     int64_t want = std::max<int64_t>(pool_bytes, std::max<int64_t>(64ll << 20,
@@ -578,7 +610,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     // ---- K1
     int k1 = 0;
     if (s->P > 0) {
-      const int tpi = std::max(1, std::min(Tc, 8));
+      const int tpi = std::max(1, std::min(Tc, 4));
       const int ntg = (Tc + tpi - 1) / tpi;
       const int64_t items = (int64_t)s->P * ntg;
       if (s->csr) {
@@ -605,22 +637,26 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
         A.n = n;
         // items of tpi tiles: enough items for dynamic balance, few enough
         // that per-item setup and work-counter atomics stay negligible
-        A.tpi = (int)std::max<int64_t>(1, std::min<int64_t>(16, (int64_t)n * Tc / (16 * warps)));
+        A.tpi = (int)std::max<int64_t>(1, std::min<int64_t>(8, (int64_t)n * Tc / (4 * warps)));
         A.tpi = std::min(A.tpi, Tc);
+        while ((int64_t)n * ((Tc + A.tpi - 1) / A.tpi) >= (int64_t(1) << 31)) A.tpi *= 2;
         A.ntg = (Tc + A.tpi - 1) / A.tpi;
         A.pct = pct;
         A.counter = l * 5 + gi;
-        if (narrow && gi == 0)
-          gate_eval<TS, unsigned, MODE, 1><<<ncta, kEvalThreads, 0, e->st>>>(Dd, C, A);
-        else if (narrow && gi == 1)
-          gate_eval<TS, unsigned, MODE, 2><<<ncta, kEvalThreads, 0, e->st>>>(Dd, C, A);
-        else if (narrow && gi == 2)
-          gate_eval<TS, unsigned, MODE, 3><<<ncta, kEvalThreads, 0, e->st>>>(Dd, C, A);
-        else if (narrow && gi == 3)
-          gate_eval<TS, unsigned, MODE, 4><<<ncta, kEvalThreads, 0, e->st>>>(Dd, C, A);
-        else
-          gate_eval<TS, long long, MODE, 0><<<ncta, kEvalThreads, 0, e->st>>>(Dd, C, A);
-        CK(cudaGetLastError());
+        const int sm = e->sms;
+        if (narrow && p100 && gi < 4) {
+          if (gi == 0) TRY((launch_eval<TS, unsigned, MODE, 1, true>(sm, e->st, Dd, C, A, ncta)));
+          if (gi == 1) TRY((launch_eval<TS, unsigned, MODE, 2, true>(sm, e->st, Dd, C, A, ncta)));
+          if (gi == 2) TRY((launch_eval<TS, unsigned, MODE, 3, true>(sm, e->st, Dd, C, A, ncta)));
+          if (gi == 3) TRY((launch_eval<TS, unsigned, MODE, 4, true>(sm, e->st, Dd, C, A, ncta)));
+        } else if (narrow && gi < 4) {
+          if (gi == 0) TRY((launch_eval<TS, unsigned, MODE, 1, false>(sm, e->st, Dd, C, A, ncta)));
+          if (gi == 1) TRY((launch_eval<TS, unsigned, MODE, 2, false>(sm, e->st, Dd, C, A, ncta)));
+          if (gi == 2) TRY((launch_eval<TS, unsigned, MODE, 3, false>(sm, e->st, Dd, C, A, ncta)));
+          if (gi == 3) TRY((launch_eval<TS, unsigned, MODE, 4, false>(sm, e->st, Dd, C, A, ncta)));
+        } else {
+          TRY((launch_eval<TS, long long, MODE, 0, false>(sm, e->st, Dd, C, A, ncta)));
+        }
         ++nl;
       }
     }
@@ -636,10 +672,10 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
       // the chunk did not fit its output regions: grow the pool, else shrink the chunk
       if (e->data_bytes - pi_bytes < room) {
         pool_bytes = std::min<int64_t>(room, (e->data_bytes - pi_bytes) * 4);
-      } else if (Wc > kWarp) {
-        Wc = std::max<int64_t>(kWarp, (wc / 2) / kWarp * kWarp);
+      } else if (Wc > kTile) {
+        Wc = std::max<int64_t>(kTile, (wc / 2) / kTile * kTile);
       } else {
-        return fail(GS_ERR_CAPACITY, "one 32-window chunk's waveforms exceed the device budget");
+        return fail(GS_ERR_CAPACITY, "one 128-window chunk's waveforms exceed the device budget");
       }
       continue;
     }
@@ -679,7 +715,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     // adapt: aim the next chunk at ~60% of the measured per-CTA region fill
     if (used > 0) {
       const double fill = (double)used / (double)part_words;
-      if (fill < 0.3 && wc == Wc) Wc = std::min<int64_t>(round_up(total, kWarp), Wc * 2);
+      if (fill < 0.3 && wc == Wc) Wc = std::min<int64_t>(round_up(total, kTile), Wc * 2);
     }
     w += wc;
   }

@@ -1,39 +1,49 @@
 // kernels.cuh -- sm_100a kernels of the windowed gate-level re-simulation path.
 //
-// Layout in HBM for one chunk of Wc cycle windows (Tc = ceil(Wc/32) tiles):
-//   cnt  [N][Tc*32] u32  toggles of net n in chunk window w
-//   tbase[N][Tc]    u64  index in `data` of the first toggle of (n, tile t);
-//                        lane j's toggles start at tbase + sum_{i<j} cnt[i]
-//   init [N][Tc]    u32  window-start value bits, bit j = window t*32+j
-//   data            TS   window-relative toggle times (u32, or u64 when a
-//                        window is longer than 2^32 fs)
-// so the 32 windows of one (net, tile) are one contiguous run of `data`:
-// a warp reading one fanin tile touches exactly the sectors holding it.
+// Layout in HBM for one chunk of Wc cycle windows, Wpad = Wc rounded up to a
+// tile of kTile = 128 windows, Tc = Wpad / 128 tiles:
+//   cnt  [N][Wpad]    u32  toggles of net n in chunk window w (0 past Wc)
+//   tbase[N][Tc]      u64  index in `data` of the first toggle of (n, tile t);
+//                          the tile's windows follow in window order, so
+//                          window w's toggles start at tbase + sum_{v<w} cnt[v]
+//   init [N][Wpad/32] u32  window-start value bits, bit j of word i = window 32i+j
+//   data              TS   window-relative toggle times (u32, or u64 when a
+//                          window is longer than 2^32 fs)
+// so the 128 windows of one (net, tile) are one contiguous run of `data`.
 //
 // Kernels
 //   K1 stim_segment_csr / stim_segment_win : cut primary-input waveforms into
 //      windows (reference StimulusSet.build + slice_windows, waveform.py:49-63,
 //      243-265), fused with the input nets' dwell/toggle sums (dwell_sweep,
 //      _kernels.py:254-295, PI rows).
-//   K4 gate_eval : one warp = one gate x 32 windows (lane = window).  Per lane
-//      the exact Algo. 1 event loop of sim_span (_kernels.py:54-210), with the
-//      window-start value (init_values, _kernels.py:213-231), the upper bound
-//      (level_ub, _kernels.py:234-251) and the dwell/toggle reduction
-//      (dwell_sweep) fused in; outputs are staged in shared memory, compacted
-//      with a warp scan and appended to a per-CTA region (no global atomics).
+//   K4 gate_eval : one warp = one gate x one 128-window tile, in three phases:
+//      (1) cooperative: coalesced loads of the fanin counts / bases / start
+//          bits, warp scans -> per-window fanin offsets, window-start input
+//          vectors (init_values, _kernels.py:213-231) and the per-window output
+//          bound (level_ub, _kernels.py:234-251) staged in shared memory;
+//      (2) one lockstep loop in which every lane with a window executes the
+//          same Algo. 1 event step of sim_span (_kernels.py:94-210); a lane
+//          whose window is exhausted pulls the next one from a shared counter,
+//          so busy windows do not leave the other lanes idle;
+//      (3) cooperative compaction: warp scan of the stored counts, one region
+//          allocation, copy out of the staging area fused with the dwell /
+//          toggle reduction (dwell_sweep, gate rows).
 //   K6 dwell_arena : dwell_sweep over a host-provided arena (compute_stats).
 //   K2 zero_delay_level : init_values seam (one level, thread per gate-window).
 #pragma once
 #include <cstdint>
 #include <climits>
 #include <cuda_runtime.h>
+#include <type_traits>
 
 namespace gs {
 
 constexpr int kWarp = 32;
-constexpr int kEvalWarps = 8;               // warps per K4 CTA
+constexpr int kTile = 128;                  // windows per (gate, tile) work unit
+constexpr int kWPL = kTile / kWarp;         // windows per lane in the cooperative phases
+constexpr int kEvalWarps = 4;               // warps per K4 CTA
 constexpr int kEvalThreads = kEvalWarps * kWarp;
-constexpr int kSlab = 512;                  // staged output timestamps per warp (smem)
+constexpr int kSlab = 1024;                 // staged output timestamps per warp (smem)
 constexpr int kMaxK = 16;                   // netlist.py:17 MAX_CELL_INPUTS
 constexpr long long kInf = LLONG_MAX;
 
@@ -46,7 +56,7 @@ enum Mode { MODE_STATS = 0, MODE_COUNTERS = 1, MODE_STORE = 3 };
 
 struct DesignDev {
   int P, G, N;
-  const int *order;            // [G] level order
+  const int *order;            // [G] level order, grouped by fanin count per level
   const int *gate_k;           // [G]
   const int *gate_pin;         // [G] first pin
   const unsigned long long *gate_lut;  // [G] k<=6: truth bits; else word offset
@@ -59,7 +69,7 @@ struct DesignDev {
 };
 
 struct ChunkDev {
-  int N, Wc, Tc, Wpad;         // nets, windows, tiles, cnt row pitch (= Tc*32)
+  int N, Wc, Tc, Wpad;         // nets, windows, 128-tiles, cnt row pitch (= Tc*128)
   long long w0;                // absolute index of the chunk's first window
   const long long *bnd;        // [W+1] absolute window boundaries
   unsigned *cnt;
@@ -93,7 +103,7 @@ struct StimDev {
 
 struct LevelArgs {
   int lo, n;                   // gates order[lo, lo+n)
-  int tpi, ntg;                // tiles per item, tile groups per gate
+  int tpi, ntg;                // 128-tiles per item, tile groups per gate
   int pct;
   int counter;                 // index into ChunkDev::work
 };
@@ -173,18 +183,36 @@ __device__ __forceinline__ void acc_flush(const ChunkDev &C, int net, long long 
   }
 }
 
+// window-start bits of the lane's 4 windows (nibble) -> the tile's 32-bit
+// words; lanes with (lane & 7) == 0 write word lane >> 3
+__device__ __forceinline__ void store_init_words(unsigned *row, int tile, unsigned nib) {
+  const unsigned lane = lane_id();
+  unsigned w = nib << ((lane & 7) * kWPL);
+  w |= __shfl_xor_sync(0xffffffffu, w, 1);
+  w |= __shfl_xor_sync(0xffffffffu, w, 2);
+  w |= __shfl_xor_sync(0xffffffffu, w, 4);
+  if ((lane & 7) == 0) row[tile * (kTile / 32) + (lane >> 3)] = w;
+}
+
+__device__ __forceinline__ uint4 ldg_u4(const unsigned *p) {
+  return __ldg(reinterpret_cast<const uint4 *>(p));
+}
+
 // ----------------------------------------------------------------- K1 (CSR)
-// One warp per (input p, group of tiles); lane = window.  cut_w is the lower
-// bound of b_w in p's sorted toggles (slice_windows, waveform.py:58); the
-// window holds toggles [cut_w, cut_{w+1}) and starts at init ^ (cut_w & 1)
-// (waveform.py:61).  Toggles land in `data` at their CSR index, so the tile
-// base is pi_off[p] + cut of lane 0 and the tile is contiguous.
+// One warp per (input p, group of 128-window tiles); lane l owns windows
+// 4l..4l+3.  cut_w = lower bound of b_w in p's sorted toggles (slice_windows,
+// waveform.py:58): one binary search per lane, then a forward scan over the
+// lane's own toggles.  Window w starts at init ^ (cut_w & 1) (waveform.py:61).
+// Toggles land in `data` at their CSR index, so the tile base is
+// pi_off[p] + cut of the tile's first window and the tile is contiguous.
 template <typename TS>
 __global__ void __launch_bounds__(256) stim_segment_csr(StimDev S, ChunkDev C, int tpi, int ntg) {
   const unsigned lane = lane_id();
   const long long nwarps = (long long)gridDim.x * (blockDim.x / kWarp);
   const long long items = (long long)S.P * ntg;
   TS *data = reinterpret_cast<TS *>(C.data);
+  const int Tw = C.Wpad / 32;
+  const long long b_end = C.bnd[C.w0 + C.Wc];  // chunk end: key of windows past Wc
   for (long long it = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
        it < items; it += nwarps) {
     const int p = (int)(it / ntg);
@@ -196,41 +224,39 @@ __global__ void __launch_bounds__(256) stim_segment_csr(StimDev S, ChunkDev C, i
     long long tc = 0, t1 = 0;
     const int t_hi = min((tg + 1) * tpi, C.Tc);
     for (int t = tg * tpi; t < t_hi; ++t) {
-      const int wr = t * kWarp + (int)lane;
-      const bool act = wr < C.Wc;
-      const long long wabs = C.w0 + wr;
-      long long b_lo = 0, b_hi = 0, cut = n;
-      if (act) {
-        b_lo = C.bnd[wabs];
-        b_hi = C.bnd[wabs + 1];
-        cut = lower_bound(seg, n, b_lo);
-      }
-      long long nxt = __shfl_down_sync(0xffffffffu, cut, 1);
-      if (act && (lane == kWarp - 1 || wr == C.Wc - 1)) nxt = lower_bound(seg, n, b_hi);
-      const unsigned c = act ? (unsigned)(nxt - cut) : 0u;
-      const unsigned v0 = act ? ((init ^ (unsigned)cut) & 1u) : 0u;
-      const unsigned word = __ballot_sync(0xffffffffu, v0);
-      const long long cut0 = __shfl_sync(0xffffffffu, cut, 0);
-      if (lane == 0) {
-        C.tbase[(size_t)p * C.Tc + t] = (unsigned long long)(off + cut0);
-        C.init[(size_t)p * C.Tc + t] = word;
-      }
-      if (act) {
-        C.cnt[(size_t)p * C.Wpad + wr] = c;
-        TS *dst = data + off + cut;
+      const int wl = t * kTile + (int)lane * kWPL;   // lane's first window (chunk-relative)
+      long long i = lower_bound(seg, n, wl < C.Wc ? C.bnd[C.w0 + wl] : b_end);
+      const long long cut0 = __shfl_sync(0xffffffffu, i, 0);
+      unsigned c[kWPL];
+      unsigned nib = 0;
+#pragma unroll
+      for (int j = 0; j < kWPL; ++j) {
+        const int wr = wl + j;
+        const bool act = wr < C.Wc;
+        const long long b_lo = act ? C.bnd[C.w0 + wr] : b_end;
+        const long long b_hi = act ? C.bnd[C.w0 + wr + 1] : b_end;
+        const long long start = i;
         long long prev = 0, acc1 = 0;
-        unsigned v = v0;
-        for (unsigned j = 0; j < c; ++j) {
-          const long long x = __ldg(seg + cut + j) - b_lo;
-          dst[j] = (TS)x;
+        unsigned v = (init ^ (unsigned)start) & 1u;
+        while (i < n && __ldg(seg + i) < b_hi) {
+          const long long x = __ldg(seg + i) - b_lo;
+          data[off + i] = (TS)x;
           if (v) acc1 += x - prev;
           v ^= 1u;
           prev = x;
+          ++i;
         }
-        if (v) acc1 += (b_hi - b_lo) - prev;
-        t1 += acc1;
-        tc += c;
+        c[j] = (unsigned)(i - start);
+        if (act) {
+          if (v) acc1 += (b_hi - b_lo) - prev;
+          t1 += acc1;
+          tc += c[j];
+          nib |= ((init ^ (unsigned)start) & 1u) << j;
+        }
       }
+      *reinterpret_cast<uint4 *>(C.cnt + (size_t)p * C.Wpad + wl) = make_uint4(c[0], c[1], c[2], c[3]);
+      if (lane == 0) C.tbase[(size_t)p * C.Tc + t] = (unsigned long long)(off + cut0);
+      store_init_words(C.init + (size_t)p * Tw, t, nib);
     }
     acc_flush(C, p, t1, tc, 0, 0, 0);
   }
@@ -238,7 +264,7 @@ __global__ void __launch_bounds__(256) stim_segment_csr(StimDev S, ChunkDev C, i
 
 // ------------------------------------------------------------ K1 (windowed)
 // Reference-constructed StimulusSet (waveform.py:235-241): per (input, window)
-// offset/count/initial are given; copy each tile into this CTA's region.
+// offset/count/initial are given; each tile is copied into this warp's region.
 template <typename TS>
 __global__ void __launch_bounds__(kEvalThreads) stim_segment_win(StimDev S, ChunkDev C, int tpi,
                                                                  int ntg) {
@@ -248,6 +274,7 @@ __global__ void __launch_bounds__(kEvalThreads) stim_segment_win(StimDev S, Chun
   unsigned long long bump = C.bump[region];
   const long long items = (long long)S.P * ntg;
   TS *data = reinterpret_cast<TS *>(C.data);
+  const int Tw = C.Wpad / 32;
   for (long long it = blockIdx.x + (long long)gridDim.x * warp; it < items;
        it += (long long)gridDim.x * kEvalWarps) {
     const int p = (int)(it / ntg);
@@ -255,42 +282,49 @@ __global__ void __launch_bounds__(kEvalThreads) stim_segment_win(StimDev S, Chun
     long long tc = 0, t1 = 0;
     const int t_hi = min((tg + 1) * tpi, C.Tc);
     for (int t = tg * tpi; t < t_hi; ++t) {
-      const int wr = t * kWarp + (int)lane;
-      const bool act = wr < C.Wc;
-      const long long wabs = C.w0 + wr;
-      unsigned c = 0, v0 = 0;
-      long long src = 0, b_lo = 0, b_hi = 0;
-      if (act) {
-        const size_t pw = (size_t)p * S.W + wabs;
-        c = (unsigned)S.counts[pw];
-        src = S.offsets[pw];
-        v0 = S.initials[pw] & 1u;
-        b_lo = C.bnd[wabs];
-        b_hi = C.bnd[wabs + 1];
+      const int wl = t * kTile + (int)lane * kWPL;
+      unsigned c[kWPL], nib = 0, s = 0;
+      long long src[kWPL];
+#pragma unroll
+      for (int j = 0; j < kWPL; ++j) {
+        const int wr = wl + j;
+        c[j] = 0;
+        src[j] = 0;
+        if (wr < C.Wc) {
+          const size_t pw = (size_t)p * S.W + C.w0 + wr;
+          c[j] = (unsigned)S.counts[pw];
+          src[j] = S.offsets[pw];
+          nib |= (S.initials[pw] & 1u) << j;
+        }
+        s += c[j];
       }
       unsigned total;
-      const unsigned ex = warp_excl_scan(c, &total);
+      const unsigned ex = warp_excl_scan(s, &total);
       const unsigned long long base = total ? region_alloc(C, bump, region, total) : 0ull;
-      const unsigned word = __ballot_sync(0xffffffffu, v0);
       const bool wrote = base != ~0ull;
-      if (lane == 0) {
-        C.tbase[(size_t)p * C.Tc + t] = wrote ? base : 0ull;
-        C.init[(size_t)p * C.Tc + t] = word;
-      }
-      if (act) {
-        C.cnt[(size_t)p * C.Wpad + wr] = wrote ? c : 0u;
+      if (lane == 0) C.tbase[(size_t)p * C.Tc + t] = wrote ? base : 0ull;
+      *reinterpret_cast<uint4 *>(C.cnt + (size_t)p * C.Wpad + wl) =
+          wrote ? make_uint4(c[0], c[1], c[2], c[3]) : make_uint4(0, 0, 0, 0);
+      store_init_words(C.init + (size_t)p * Tw, t, nib);
+      unsigned long long o = base + ex;
+#pragma unroll
+      for (int j = 0; j < kWPL; ++j) {
+        const int wr = wl + j;
+        if (wr >= C.Wc) continue;
+        const long long b_lo = C.bnd[C.w0 + wr], b_hi = C.bnd[C.w0 + wr + 1];
         long long prev = 0, acc1 = 0;
-        unsigned v = v0;
-        for (unsigned j = 0; j < c; ++j) {
-          const long long x = __ldg(S.buf + src + j) - b_lo;
-          if (wrote) data[base + ex + j] = (TS)x;
+        unsigned v = (nib >> j) & 1u;
+        for (unsigned q = 0; q < c[j]; ++q) {
+          const long long x = __ldg(S.buf + src[j] + q) - b_lo;
+          if (wrote) data[o + q] = (TS)x;
           if (v) acc1 += x - prev;
           v ^= 1u;
           prev = x;
         }
         if (v) acc1 += (b_hi - b_lo) - prev;
         t1 += acc1;
-        tc += c;
+        tc += c[j];
+        o += c[j];
       }
     }
     acc_flush(C, p, t1, tc, 0, 0, 0);
@@ -299,7 +333,6 @@ __global__ void __launch_bounds__(kEvalThreads) stim_segment_win(StimDev S, Chun
 }
 
 // ------------------------------------------------------------------- K4
-// Algo. 1 for one gate over one 32-window tile; lane = window.
 //   K > 0 : fanin count fixed at compile time (fully unrolled, registers);
 //   K == 0: generic k <= 16 (runtime loops).
 //   TT    : time arithmetic -- unsigned (narrow: every window length plus the
@@ -328,101 +361,140 @@ __device__ __forceinline__ long long arc_delay<long long>(const DesignDev &D, in
   return __ldg(D.arc + (size_t)row * 2 + col);
 }
 
-template <typename TS, typename TT, int MODE, int K>
-__device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C, int g, int k,
-                                          unsigned long long lut, const int *net,
-                                          const TT *ic, const int *arc, int t, int pct,
-                                          TS *slab, unsigned long long &bump,
-                                          unsigned long long region, long long &acc_t1,
-                                          long long &acc_tc, long long &acc_filt,
-                                          long long &acc_icf, long long &acc_disc) {
+// per-warp shared-memory tile state
+template <typename TS, typename TT, int KM>
+struct TileSmem {
+  TS slab[kSlab];                  // staged fanin segments, then output staging
+  // the item's condition tables (narrow kernels): arcs[(p << (KM-1) | row) * 2 + col]
+  unsigned arcs[KM <= 4 ? KM * (1 << (KM - 1)) * 2 : 1];
+  unsigned offs[KM][kTile + 1];    // per pin: window w's toggles start at offs[p][w]
+  unsigned ubo[kTile + 1];         // output staging offsets: prefix of the per-window bound
+  TT wlen[kTile];                  // window lengths
+  unsigned cnt[kTile];             // stored toggles per window
+  unsigned short idx0[kTile];      // window-start input vector
+  unsigned char y0[kTile];         // window-start output value
+  unsigned next;                   // dynamic window counter
+};
+
+// Phase 2 of K4: one lockstep loop over the tile's windows.  Every lane with
+// a window executes the same event step of sim_span (_kernels.py:94-203); a
+// lane whose window is exhausted records it and pulls the next window from the
+// shared counter, so busy windows do not leave the other lanes idle.
+//   SMEM   : fanin segments and output staging live in the warp's smem slab
+//            (else fanins are read in place and outputs staged in the pool);
+//   PCT100 : pathpulse 100 % -- the threshold is the delay itself, and stored
+//            edges are never retracted, so the retraction target is a register.
+template <typename TS, typename TT, int MODE, int K, bool PCT100, bool SMEM>
+__device__ __forceinline__ void event_loop(
+    const DesignDev &D, const ChunkDev &C, int g, int kk, unsigned long long lut, const TT *ic,
+    const int *arc, int pct, TileSmem<TS, TT, (K > 0 ? K : kMaxK)> &S,
+    const typename std::conditional<SMEM, unsigned, const TS *>::type *inb, TS *stage, bool ok,
+    int base_w, int nact, long long &acc_tc, long long &acc_filt, long long &acc_icf,
+    long long &acc_disc) {
   constexpr int KM = K > 0 ? K : kMaxK;
-  const int kk = K > 0 ? K : k;
+  constexpr bool ARC_SMEM = K > 0 && K <= 4 && sizeof(TT) == 4;
+  constexpr int ROWS = K > 0 ? 1 << (K - 1) : 1;
   const TT INF = TimeTraits<TT>::inf();
-  const unsigned lane = lane_id();
-  const int wr = t * kWarp + (int)lane;
-  const bool act = wr < C.Wc;
-  const long long wabs = C.w0 + wr;
-  TS *data = reinterpret_cast<TS *>(C.data);
-  long long b_lo = 0, wlen64 = 0;
-  if (act) {
-    b_lo = C.bnd[wabs];
-    wlen64 = C.bnd[wabs + 1] - b_lo;
-  }
-  const TT wlen = (TT)wlen64;
-
-  // fanin tiles: counts, bases, window-start bits (init_values + level_ub fused)
-  const TS *sp[KM];
-  unsigned n[KM];
-  unsigned idx = 0, ub = 0;
-#pragma unroll
-  for (int p = 0; p < kk; ++p) {
-    const int nn = net[p];
-    const unsigned c = act ? __ldg(C.cnt + (size_t)nn * C.Wpad + wr) : 0u;
-    const unsigned long long tb = __ldg(C.tbase + (size_t)nn * C.Tc + t);
-    const unsigned iw = __ldg(C.init + (size_t)nn * C.Tc + t);
-    unsigned tot;
-    const unsigned ex = warp_excl_scan(c, &tot);
-    sp[p] = data + tb + ex;
-    n[p] = c;
-    ub += c;
-    idx |= ((iw >> lane) & 1u) << p;
-  }
-  const unsigned y0 = act ? lut_bit(lut, kk, D.lut_words, idx) : 0u;
-
-  // output staging: smem slab when the tile's bound fits, else this warp's region
-  unsigned UB;
-  const unsigned ubx = warp_excl_scan(ub, &UB);
-  TS *st;
-  bool ok = true;
-  if (UB <= (unsigned)kSlab) {
-    st = slab + ubx;
-  } else {
-    const unsigned long long sb = region_alloc(C, bump, region, UB);
-    ok = sb != ~0ull;
-    st = data + (ok ? sb : 0ull) + ubx;
-  }
-
-  // ---- per-lane event loop (sim_span, _kernels.py:94-203)
-  unsigned pos[KM];
-  TT nxt[KM];
-#pragma unroll
-  for (int p = 0; p < kk; ++p) { pos[p] = 0; nxt[p] = INF; }
-  unsigned need = (act && ok) ? ((1u << kk) - 1u) : 0u;
-  unsigned y = y0;
-  int cnt = 0, peak = 0, filt = 0, icf = 0, disc = 0;
+  unsigned l_tc = 0, l_filt = 0, l_icf = 0, l_disc = 0;
+  int w = -1;
+  bool has = false, more = ok;
+  unsigned cur[KM], end[KM], need = 0, idx = 0, y = 0, y0 = 0, so = 0;
+  TT nxt[KM], wlen = 0, t_last = 0, t_stored = 0;
+  int cnt = 0, peak = 0, filt = 0, icf = 0, disc = 0, cap = 0;
   bool has_last = false, last_stored = false;
-  TT t_last = 0;
-  const int cap = (int)ub;  // peak <= #events <= sum of fanin toggles
+  auto in_at = [&](int p, unsigned q) -> TT {
+    if constexpr (SMEM) return (TT)S.slab[inb[p] + q];
+    else return (TT)__ldg(inb[p] + q);
+  };
   while (true) {
+    if (!has && more) {
+      const unsigned nw = atomicAdd(&S.next, 1u);
+      if (nw < (unsigned)nact) {
+        w = (int)nw;
+        has = true;
+#pragma unroll
+        for (int p = 0; p < kk; ++p) {
+          cur[p] = S.offs[p][w];
+          end[p] = S.offs[p][w + 1];
+          nxt[p] = INF;
+        }
+        idx = S.idx0[w];
+        y0 = y = lut_bit(lut, kk, D.lut_words, idx);
+        wlen = S.wlen[w];
+        so = S.ubo[w];
+        cap = (int)(S.ubo[w + 1] - so);  // peak <= #events <= fanin toggles
+        need = (1u << kk) - 1u;
+        cnt = peak = filt = icf = disc = 0;
+        has_last = last_stored = false;
+      } else {
+        more = false;
+      }
+    }
+    if (!__any_sync(0xffffffffu, has)) break;
+    if (!has) continue;
     TT tmin = INF;
 #pragma unroll
     for (int p = 0; p < kk; ++p) {
       if ((need >> p) & 1u) {
         // interconnect inertial filter: drop adjacent pairs narrower than d
         const TT d = ic[p];
-        unsigned q = pos[p];
-        const TS *s = sp[p];
+        unsigned q = cur[p];
         if (d > 0) {
-          while (q + 1 < n[p] && (TT)__ldg(s + q + 1) - (TT)__ldg(s + q) < d) {
+          while (q + 1 < end[p] && in_at(p, q + 1) - in_at(p, q) < d) {
             q += 2;
             ++icf;
           }
         }
-        pos[p] = q;
-        nxt[p] = q < n[p] ? (TT)__ldg(s + q) + d : INF;
+        cur[p] = q;
+        nxt[p] = q < end[p] ? in_at(p, q) + d : INF;
       }
       tmin = min(tmin, nxt[p]);
     }
-    if (tmin == INF) break;
+    TS *st = stage + so;
+    if (tmin == INF) {
+      // window exhausted: flush the pending edge, record the window
+      if (has_last && last_stored) {
+        if (cnt < cap) st[cnt] = (TS)t_last; else atomicExch(C.err + ERR_CAP, 1);
+        ++cnt;
+        peak = max(peak, cnt);
+      }
+      S.cnt[w] = (unsigned)cnt;
+      S.y0[w] = (unsigned char)y0;
+      l_tc += cnt;
+      l_filt += filt;
+      l_icf += icf;
+      l_disc += disc;
+      const int wr = base_w + w;
+      if (MODE & MODE_COUNTERS) {
+        const size_t gw = (size_t)g * C.Wpad + wr;
+        C.a_cnt[gw] = cnt;
+        C.a_peak[gw] = peak;
+        C.a_filt[gw] = filt;
+        C.a_icf[gw] = icf;
+        C.a_disc[gw] = disc;
+        C.a_init[gw] = (unsigned char)y0;
+      }
+      if ((MODE & MODE_STORE) == MODE_STORE) {
+        // store pass: the (g, w) region of the reference arena layout gets
+        // every slot the lane ever wrote, [0, peak) (waveform.py:340-345)
+        const long long o = C.a_off[(size_t)g * C.Wpad + wr];
+        const long long b_lo = C.bnd[C.w0 + wr];
+        if (o >= 0 && o + peak <= C.a_nbuf) {
+          for (int j = 0; j < peak; ++j) C.a_buf[o + j] = (long long)st[j] + b_lo;
+        } else if (peak) {
+          atomicExch(C.err + ERR_CAP, 1);
+        }
+      }
+      has = false;
+      continue;
+    }
     // multiple simultaneous inputs: consume every pin arriving at tmin
     unsigned sw = 0;
 #pragma unroll
     for (int p = 0; p < kk; ++p) {
-      if (nxt[p] == tmin) {
-        pos[p] += 1;
-        sw |= 1u << p;
-      }
+      const bool hit = nxt[p] == tmin;
+      cur[p] += hit ? 1u : 0u;
+      sw |= (hit ? 1u : 0u) << p;
     }
     idx ^= sw;
     need = sw;
@@ -435,121 +507,213 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
       for (int p = 0; p < kk; ++p) {
         if ((sw >> p) & 1u) {
           const int row = (int)((idx & ((1u << p) - 1u)) | ((idx >> (p + 1)) << p));
-          dly = max(dly, arc_delay<TT>(D, arc[p] + row, col));
+          if constexpr (ARC_SMEM)
+            dly = max(dly, (TT)S.arcs[((p * ROWS) + row) * 2 + col]);
+          else
+            dly = max(dly, arc_delay<TT>(D, arc[p] + row, col));
         }
       }
       const TT t_out = tmin + dly;
-      const TT thr = (TT)((unsigned long long)dly * (unsigned)pct / 100u);
+      const TT thr = PCT100 ? dly : (TT)((unsigned long long)dly * (unsigned)pct / 100u);
       const bool have = has_last || cnt > 0;
-      const TT tgt = has_last ? t_last : (cnt > 0 ? (TT)st[cnt - 1] : (TT)0);
+      const TT tgt = has_last ? t_last : t_stored;
       if (have && (t_out <= tgt || t_out - tgt < thr)) {
         // inertial rejection: the pulse is cancelled in full
         if (has_last) {
           if (!last_stored) --disc;
           has_last = false;
         } else {
+          // pops a stored edge (only below 100 %); its predecessor becomes
+          // the retraction target
           --cnt;
+          if (!PCT100 && cnt > 0) t_stored = (TT)st[cnt - 1];
         }
         ++filt;
       } else {
         if (has_last && last_stored) {
           if (cnt < cap) st[cnt] = (TS)t_last; else atomicExch(C.err + ERR_CAP, 1);
+          t_stored = t_last;
           ++cnt;
           peak = max(peak, cnt);
         }
-        if (t_out < wlen) {
-          last_stored = true;
-        } else {
-          ++disc;  // lands at or past the window end
-          last_stored = false;
-        }
+        last_stored = t_out < wlen;  // else: lands at or past the window end
+        disc += last_stored ? 0 : 1;
         has_last = true;
         t_last = t_out;
       }
       y = ny;
     }
   }
-  if (has_last && last_stored) {
-    if (cnt < cap) st[cnt] = (TS)t_last; else atomicExch(C.err + ERR_CAP, 1);
-    ++cnt;
-    peak = max(peak, cnt);
-  }
-  if (!(act && ok)) cnt = peak = 0;
+  acc_tc += l_tc;
+  acc_filt += l_filt;
+  acc_icf += l_icf;
+  acc_disc += l_disc;
+}
 
-  // ---- compaction: warp scan of counts, one region allocation per tile;
+template <typename TS, typename TT, int MODE, int K, bool PCT100>
+__device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C, int g, int k,
+                                          unsigned long long lut, const int *net,
+                                          const TT *ic, const int *arc, int t, int pct,
+                                          TileSmem<TS, TT, (K > 0 ? K : kMaxK)> &S,
+                                          unsigned long long &bump, unsigned long long region,
+                                          long long &acc_t1, long long &acc_tc,
+                                          long long &acc_filt, long long &acc_icf,
+                                          long long &acc_disc) {
+  constexpr int KM = K > 0 ? K : kMaxK;
+  const int kk = K > 0 ? K : k;
+  const TT INF = TimeTraits<TT>::inf();
+  const unsigned lane = lane_id();
+  const int base_w = t * kTile;
+  const int nact = min(kTile, C.Wc - base_w);
+  const int wl = (int)lane * kWPL;
+  const int Tw = C.Wpad / 32;
+  TS *data = reinterpret_cast<TS *>(C.data);
+
+  // ---- phase 1: fanin tiles -> per-window offsets, start vectors, bounds
+  unsigned long long tb[KM];
+  unsigned tot[KM];
+  unsigned ub[kWPL] = {0, 0, 0, 0};
+  unsigned ix[kWPL] = {0, 0, 0, 0};
+#pragma unroll
+  for (int p = 0; p < kk; ++p) {
+    const int nn = net[p];
+    const uint4 c = ldg_u4(C.cnt + (size_t)nn * C.Wpad + base_w + wl);
+    const unsigned ex = warp_excl_scan(c.x + c.y + c.z + c.w, &tot[p]);
+    S.offs[p][wl] = ex;
+    S.offs[p][wl + 1] = ex + c.x;
+    S.offs[p][wl + 2] = ex + c.x + c.y;
+    S.offs[p][wl + 3] = ex + c.x + c.y + c.z;
+    if (lane == kWarp - 1) S.offs[p][kTile] = tot[p];
+    tb[p] = __ldg(C.tbase + (size_t)nn * C.Tc + t);
+    const unsigned nib = (__ldg(C.init + (size_t)nn * Tw + t * (kTile / 32) + (lane >> 3)) >>
+                          ((lane & 7) * kWPL)) & 0xfu;
+#pragma unroll
+    for (int j = 0; j < kWPL; ++j) ix[j] |= ((nib >> j) & 1u) << p;
+    ub[0] += c.x;
+    ub[1] += c.y;
+    ub[2] += c.z;
+    ub[3] += c.w;
+  }
+  unsigned UB;
+  const unsigned ux = warp_excl_scan(ub[0] + ub[1] + ub[2] + ub[3], &UB);
+  S.ubo[wl] = ux;
+  S.ubo[wl + 1] = ux + ub[0];
+  S.ubo[wl + 2] = ux + ub[0] + ub[1];
+  S.ubo[wl + 3] = ux + ub[0] + ub[1] + ub[2];
+  if (lane == kWarp - 1) S.ubo[kTile] = UB;
+#pragma unroll
+  for (int j = 0; j < kWPL; ++j) {
+    S.idx0[wl + j] = (unsigned short)ix[j];
+    const int wr = base_w + wl + j;
+    S.wlen[wl + j] = wr < C.Wc ? (TT)(C.bnd[C.w0 + wr + 1] - C.bnd[C.w0 + wr]) : (TT)0;
+  }
+  if (lane == 0) S.next = 0;
+  // Staging: fanin segments (UB words) then outputs (UB words) in the smem
+  // slab when 2 * UB fits; otherwise inputs are read in place and outputs go
+  // to this warp's region of the pool.
+  const bool in_smem = 2 * UB <= (unsigned)kSlab;
+  unsigned inb_off[KM];            // smem: pin p's tile segment starts at slab[inb_off[p]]
+  const TS *inb_glob[KM];          // else: read in place
+  TS *stage;
+  bool ok = true;
+  if (in_smem) {
+    unsigned o = 0;
+#pragma unroll
+    for (int p = 0; p < kk; ++p) {
+      const TS *src = data + tb[p];
+      for (unsigned i = lane; i < tot[p]; i += kWarp) S.slab[o + i] = __ldg(src + i);
+      inb_off[p] = o;
+      o += tot[p];
+    }
+    stage = S.slab + UB;
+  } else {
+#pragma unroll
+    for (int p = 0; p < kk; ++p) inb_glob[p] = data + tb[p];
+    const unsigned long long sb = region_alloc(C, bump, region, UB);
+    ok = sb != ~0ull;
+    stage = data + (ok ? sb : 0ull);
+    if (!ok) {  // pool full: the chunk is re-run; record empty windows meanwhile
+#pragma unroll
+      for (int j = 0; j < kWPL; ++j) S.cnt[wl + j] = 0;
+    }
+  }
+  __syncwarp();
+
+  // ---- phase 2: one lockstep loop (see event_loop)
+  if (in_smem) {
+    event_loop<TS, TT, MODE, K, PCT100, true>(D, C, g, kk, lut, ic, arc, pct, S, inb_off, stage,
+                                              ok, base_w, nact, acc_tc, acc_filt, acc_icf,
+                                              acc_disc);
+  } else {
+    event_loop<TS, TT, MODE, K, PCT100, false>(D, C, g, kk, lut, ic, arc, pct, S, inb_glob,
+                                               stage, ok, base_w, nact, acc_tc, acc_filt,
+                                               acc_icf, acc_disc);
+  }
+  __syncwarp();
+
+  // ---- phase 3: compaction (warp scan of the lane's 4 windows' counts);
   // the copy out of the staging area also yields the dwell at 1 (dwell_sweep)
+  unsigned c[kWPL], nib = 0, s = 0;
+#pragma unroll
+  for (int j = 0; j < kWPL; ++j) {
+    const bool act = wl + j < nact;
+    c[j] = act ? S.cnt[wl + j] : 0u;
+    nib |= (act ? (unsigned)S.y0[wl + j] : 0u) << j;
+    s += c[j];
+  }
   unsigned CNT;
-  const unsigned cx = warp_excl_scan((unsigned)cnt, &CNT);
+  const unsigned cx = warp_excl_scan(s, &CNT);
   const unsigned long long ob = CNT ? region_alloc(C, bump, region, CNT) : 0ull;
   const bool wrote = ob != ~0ull;  // else the chunk is re-run; keep readers in bounds
-  const unsigned word = __ballot_sync(0xffffffffu, y0);
   const int gnet = D.P + g;
-  if (lane == 0) {
-    C.tbase[(size_t)gnet * C.Tc + t] = wrote ? ob : 0ull;
-    C.init[(size_t)gnet * C.Tc + t] = word;
-  }
-  if (act) {
-    C.cnt[(size_t)gnet * C.Wpad + wr] = wrote ? (unsigned)cnt : 0u;
-    TS *dst = data + (wrote ? ob + cx : 0ull);
-    unsigned v = y0;
-    long long prev = 0, t1 = 0;
-    for (int j = 0; j < cnt; ++j) {
-      const TS x = st[j];
-      if (wrote) dst[j] = x;
+  if (lane == 0) C.tbase[(size_t)gnet * C.Tc + t] = wrote ? ob : 0ull;
+  *reinterpret_cast<uint4 *>(C.cnt + (size_t)gnet * C.Wpad + base_w + wl) =
+      wrote ? make_uint4(c[0], c[1], c[2], c[3]) : make_uint4(0, 0, 0, 0);
+  store_init_words(C.init + (size_t)gnet * Tw, t, nib);
+  TS *dst = data + (wrote ? ob + cx : 0ull);
+  long long t1 = 0;
+#pragma unroll
+  for (int j = 0; j < kWPL; ++j) {
+    if (wl + j >= nact) continue;
+    const TS *src = stage + S.ubo[wl + j];
+    unsigned v = (nib >> j) & 1u;
+    long long prev = 0;
+    for (unsigned q = 0; q < c[j]; ++q) {
+      const TS x = src[q];
+      if (wrote) dst[q] = x;
       if (v) t1 += (long long)x - prev;
       v ^= 1u;
       prev = (long long)x;
     }
-    if (v) t1 += wlen64 - prev;
-    acc_t1 += t1;
-    acc_tc += cnt;
-    acc_filt += filt;
-    acc_icf += icf;
-    acc_disc += disc;
-    if (MODE & MODE_COUNTERS) {
-      const size_t gw = (size_t)g * C.Wpad + wr;
-      C.a_cnt[gw] = cnt;
-      C.a_peak[gw] = peak;
-      C.a_filt[gw] = filt;
-      C.a_icf[gw] = icf;
-      C.a_disc[gw] = disc;
-      C.a_init[gw] = (unsigned char)y0;
-    }
-    if ((MODE & MODE_STORE) == MODE_STORE) {
-      // store pass: the (g, w) region of the reference arena layout receives
-      // every slot the lane ever wrote, [0, peak) (waveform.py:340-345)
-      const long long o = C.a_off[(size_t)g * C.Wpad + wr];
-      if (o >= 0 && o + peak <= C.a_nbuf) {
-        for (int j = 0; j < peak; ++j) C.a_buf[o + j] = (long long)st[j] + b_lo;
-      } else if (peak) {
-        atomicExch(C.err + ERR_CAP, 1);
-      }
-    }
+    if (v) t1 += (long long)S.wlen[wl + j] - prev;
+    dst += c[j];
   }
+  acc_t1 += t1;
   __syncwarp();
 }
 
 // One launch per (logic level, fanin-count group); the level barrier is the
 // launch boundary.  Persistent grid with dynamic work fetching: each warp takes
-// the next item (gate, group of tpi tiles) from a per-launch counter, and owns
+// the next item (gate, group of tpi tiles) from a per-launch counter and owns
 // a private output region (no CTA barrier, no global atomics on the data path).
-template <typename TS, typename TT, int MODE, int K>
-__global__ void __launch_bounds__(kEvalThreads) gate_eval(DesignDev D, ChunkDev C, LevelArgs A) {
+template <typename TS, typename TT, int MODE, int K, bool PCT100>
+__global__ void __launch_bounds__(kEvalThreads, 6) gate_eval(DesignDev D, ChunkDev C, LevelArgs A) {
   constexpr int KM = K > 0 ? K : kMaxK;
-  __shared__ TS s_slab[kEvalWarps][kSlab];
+  using SM = TileSmem<TS, TT, KM>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x / kWarp;
+  SM &S = reinterpret_cast<SM *>(smem_raw)[warp];
   const unsigned lane = lane_id();
   const unsigned long long region = (unsigned long long)blockIdx.x * kEvalWarps + warp;
   unsigned long long bump = C.bump[region];
-  const long long items = (long long)A.n * A.ntg;
-  TS *slab = s_slab[warp];
+  const unsigned items = (unsigned)A.n * (unsigned)A.ntg;
   while (true) {
-    long long it = 0;
-    if (lane == 0) it = (long long)atomicAdd(C.work + A.counter, 1u);
+    unsigned it = 0;
+    if (lane == 0) it = atomicAdd(C.work + A.counter, 1u);
     it = __shfl_sync(0xffffffffu, it, 0);
     if (it >= items) break;
-    const int j = (int)(it / A.ntg);
-    const int tg = (int)(it % A.ntg);
+    const int j = (int)(it / (unsigned)A.ntg);
+    const int tg = (int)(it % (unsigned)A.ntg);
     const int g = __ldg(D.order + A.lo + j);
     const int k = K > 0 ? K : __ldg(D.gate_k + g);
     const int pin0 = __ldg(D.gate_pin + g);
@@ -564,13 +728,27 @@ __global__ void __launch_bounds__(kEvalThreads) gate_eval(DesignDev D, ChunkDev 
       ic[p] = (TT)__ldg(D.pin_ic + pin0 + p);
       arc[p] = __ldg(D.pin_arc + pin0 + p);
     }
+    if (K > 0 && K <= 4 && sizeof(TT) == 4) {
+      // condition tables of this gate -> smem: arcs[(p << (K-1) | row) * 2 + col]
+      constexpr int R = K > 0 ? 1 << (K - 1) : 1;
+      for (int i = (int)lane; i < (K > 0 ? K : 1) * R * 2; i += kWarp) {
+        const int pp = i / (2 * R), rc = i % (2 * R);
+        S.arcs[i] = __ldg(D.arc32 + (size_t)arc[pp] * 2 + rc);
+      }
+      __syncwarp();
+    }
     long long t1 = 0, tc = 0, filt = 0, icf = 0, disc = 0;
     for (int t = t_lo; t < t_hi; ++t)
-      eval_tile<TS, TT, MODE, K>(D, C, g, k, lut, net, ic, arc, t, A.pct, slab, bump, region,
-                                 t1, tc, filt, icf, disc);
+      eval_tile<TS, TT, MODE, K, PCT100>(D, C, g, k, lut, net, ic, arc, t, A.pct, S, bump,
+                                         region, t1, tc, filt, icf, disc);
     acc_flush(C, D.P + g, t1, tc, filt, icf, disc);
   }
   if (lane == 0) C.bump[region] = bump;
+}
+
+template <typename TS, typename TT, int K>
+constexpr size_t eval_smem_bytes() {
+  return sizeof(TileSmem<TS, TT, (K > 0 ? K : kMaxK)>) * kEvalWarps;
 }
 
 // chunk accumulators -> run accumulators [t1 | tc | ig | filtered, icf, disc]
@@ -672,7 +850,7 @@ __global__ void dwell_arena(DwellArgs A) {
 }
 
 // ------------------------------------------------------------------- K2
-// init_values (_kernels.py:213-231) for one level: vals[out][w] = lut[idx].
+// init_values (_kernels.py:213-231) for one level: vals[P+g][w] = lut[idx].
 __global__ void zero_delay_level(DesignDev D, unsigned char *vals, long long W, int lo, int n) {
   const long long total = (long long)n * W;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
