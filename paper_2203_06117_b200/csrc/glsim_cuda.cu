@@ -511,10 +511,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
   const int nregions = ncta * kEvalWarps;
   if (nregions > e->ncta_cap) {
     dfree(e->bump);
-    if (e->bump_host) cudaFreeHost(e->bump_host);
-    e->bump_host = nullptr;
-    TRY(dalloc(&e->bump, nregions));
-    CK(cudaMallocHost((void **)&e->bump_host, sizeof(unsigned long long) * nregions));
+    TRY(dalloc(&e->bump, 2 * (size_t)nregions + 1));  // slot states + block counter
     e->ncta_cap = nregions;
   }
   if (e->work_cap < D->L * 5 + 1) {
@@ -567,7 +564,10 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     want = std::min(want, room);
     TRY(ensure_data(e, pi_bytes + want));
     const int64_t pool_words = (e->data_bytes - pi_bytes) / (int64_t)sizeof(TS);
-    const int64_t part_words = pool_words / nregions;
+    // blocks: small enough that the partially used block of every slot wastes
+    // at most ~1/4 of the pool, large enough that block grabs stay rare
+    const int64_t block_words =
+        std::max<int64_t>(256, std::min<int64_t>(1 << 16, pool_words / (4 * (int64_t)nregions)));
 
     ChunkDev C;
     memset(&C, 0, sizeof(C));
@@ -582,8 +582,10 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     C.init = e->init;
     C.data = e->data;
     C.pool_base = (unsigned long long)(pi_bytes / (int64_t)sizeof(TS));
-    C.part_words = (unsigned long long)part_words;
+    C.block_words = (unsigned long long)block_words;
+    C.pool_blocks = (unsigned long long)(pool_words / block_words);
     C.bump = e->bump;
+    C.blk_next = e->bump + 2 * (size_t)nregions;
     C.work = e->work;
     C.acc = e->acc;
     C.err = e->err;
@@ -603,7 +605,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
       }
     }
     CK(cudaMemsetAsync(e->acc, 0, sizeof(long long) * ACC_ROWS * N, e->st));
-    CK(cudaMemsetAsync(e->bump, 0, sizeof(unsigned long long) * nregions, e->st));
+    CK(cudaMemsetAsync(e->bump, 0, sizeof(unsigned long long) * (2 * (size_t)nregions + 1), e->st));
     CK(cudaMemsetAsync(e->work, 0, sizeof(unsigned) * (D->L * 5 + 1), e->st));
     CK(cudaMemsetAsync(e->err, 0, sizeof(int) * ERR_NFLAGS, e->st));
     CK(cudaEventRecord(e->ev[0], e->st));
@@ -662,7 +664,8 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     }
     CK(cudaEventRecord(e->ev[2], e->st));
     CK(cudaMemcpyAsync(e->err_host, e->err, sizeof(int) * ERR_NFLAGS, cudaMemcpyDeviceToHost, e->st));
-    CK(cudaMemcpyAsync(e->bump_host, e->bump, sizeof(unsigned long long) * nregions,
+    unsigned long long blocks_used = 0;
+    CK(cudaMemcpyAsync(&blocks_used, e->bump + 2 * (size_t)nregions, sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, e->st));
     CK(cudaStreamSynchronize(e->st));
     if (e->err_host[ERR_CAP])
@@ -679,9 +682,8 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
       }
       continue;
     }
-    unsigned long long used = 0;
-    for (int c = 0; c < nregions; ++c) used = std::max(used, e->bump_host[c]);
-    peak_bytes = std::max<int64_t>(peak_bytes, (int64_t)(used * nregions * sizeof(TS)) + pi_bytes);
+    const int64_t used_words = (int64_t)blocks_used * block_words;
+    peak_bytes = std::max<int64_t>(peak_bytes, used_words * (int64_t)sizeof(TS) + pi_bytes);
     float a = 0.f, b = 0.f;
     CK(cudaEventElapsedTime(&a, e->ev[0], e->ev[1]));
     CK(cudaEventElapsedTime(&b, e->ev[1], e->ev[2]));
@@ -713,8 +715,8 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
       CK(cudaStreamSynchronize(e->st));
     }
     // adapt: aim the next chunk at ~60% of the measured per-CTA region fill
-    if (used > 0) {
-      const double fill = (double)used / (double)part_words;
+    if (used_words > 0) {
+      const double fill = (double)used_words / (double)pool_words;
       if (fill < 0.3 && wc == Wc) Wc = std::min<int64_t>(round_up(total, kTile), Wc * 2);
     }
     w += wc;

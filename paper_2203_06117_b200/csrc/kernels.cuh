@@ -76,8 +76,11 @@ struct ChunkDev {
   unsigned long long *tbase;
   unsigned *init;
   void *data;                  // TS[]
-  unsigned long long pool_base, part_words;  // per-warp regions of `data`
-  unsigned long long *bump;    // [gridDim.x * kEvalWarps] words used in each region
+  unsigned long long pool_base;   // first word of the gate-output pool in `data`
+  unsigned long long block_words, pool_blocks;  // the pool is handed out in blocks
+  unsigned long long *blk_next;  // blocks handed out so far
+  unsigned long long *bump;    // [2 * regions]: per (CTA, warp) slot, next free word of
+                               // its current block and words left in it
   unsigned *work;              // per-launch work counters (dynamic item fetch)
   long long *acc;              // [ACC_ROWS][N]
   int *err;                    // [ERR_NFLAGS]
@@ -148,20 +151,51 @@ __device__ __forceinline__ long long lower_bound(const long long *__restrict__ a
   return lo;
 }
 
-// bump-allocate `words` (warp-uniform) in this warp's private region of the
-// pool; returns the absolute index in `data` (same on all lanes) or ~0ull when
-// the region is full (the chunk is then re-run with more room)
-__device__ __forceinline__ unsigned long long region_alloc(const ChunkDev &C,
-                                                           unsigned long long &bump,
-                                                           unsigned long long region,
-                                                           unsigned long long words) {
-  const unsigned long long old = bump;
-  if (old + words > C.part_words) {
-    if (lane_id() == 0) atomicExch(C.err + ERR_POOL, 1);
-    return ~0ull;
+// Output space: each (CTA, warp) slot bump-allocates from its current block of
+// the pool and takes a fresh run of blocks (one global atomic) when the block
+// is exhausted; slot state persists across the launches of a chunk.  All
+// arguments are warp-uniform; returns the absolute index in `data` (same on
+// all lanes) or ~0ull when the pool is exhausted (the chunk is then re-run
+// with more room).
+struct Region {
+  unsigned long long next, left;
+  unsigned long long slot;
+};
+
+__device__ __forceinline__ Region region_open(const ChunkDev &C, unsigned long long slot) {
+  Region R;
+  R.slot = slot;
+  R.next = C.bump[2 * slot];
+  R.left = C.bump[2 * slot + 1];
+  return R;
+}
+
+__device__ __forceinline__ void region_close(const ChunkDev &C, const Region &R) {
+  if (lane_id() == 0) {
+    C.bump[2 * R.slot] = R.next;
+    C.bump[2 * R.slot + 1] = R.left;
   }
-  bump = old + words;
-  return C.pool_base + region * C.part_words + old;
+}
+
+__device__ __forceinline__ unsigned long long region_alloc(const ChunkDev &C, Region &R,
+                                                           unsigned long long words) {
+  if (words > R.left) {
+    const unsigned long long nb = (words + C.block_words - 1) / C.block_words;
+    unsigned long long first = 0;
+    if (lane_id() == 0) first = atomicAdd(C.blk_next, nb);
+    first = __shfl_sync(0xffffffffu, first, 0);
+    if (first + nb > C.pool_blocks) {
+      if (lane_id() == 0) atomicExch(C.err + ERR_POOL, 1);
+      R.left = 0;
+      return ~0ull;
+    }
+    R.next = C.pool_base + first * C.block_words;
+    R.left = nb * C.block_words;
+  }
+  const unsigned long long at = R.next;
+  R.next += words;
+  R.left -= words;
+  return at;
 }
 
 // warp-wide sum of five per-lane partials, added by lane 0 into acc[row][net]
@@ -270,8 +304,7 @@ __global__ void __launch_bounds__(kEvalThreads) stim_segment_win(StimDev S, Chun
                                                                  int ntg) {
   const unsigned lane = lane_id();
   const int warp = threadIdx.x / kWarp;
-  const unsigned long long region = (unsigned long long)blockIdx.x * kEvalWarps + warp;
-  unsigned long long bump = C.bump[region];
+  Region R = region_open(C, (unsigned long long)blockIdx.x * kEvalWarps + warp);
   const long long items = (long long)S.P * ntg;
   TS *data = reinterpret_cast<TS *>(C.data);
   const int Tw = C.Wpad / 32;
@@ -300,7 +333,7 @@ __global__ void __launch_bounds__(kEvalThreads) stim_segment_win(StimDev S, Chun
       }
       unsigned total;
       const unsigned ex = warp_excl_scan(s, &total);
-      const unsigned long long base = total ? region_alloc(C, bump, region, total) : 0ull;
+      const unsigned long long base = total ? region_alloc(C, R, total) : 0ull;
       const bool wrote = base != ~0ull;
       if (lane == 0) C.tbase[(size_t)p * C.Tc + t] = wrote ? base : 0ull;
       *reinterpret_cast<uint4 *>(C.cnt + (size_t)p * C.Wpad + wl) =
@@ -329,7 +362,7 @@ __global__ void __launch_bounds__(kEvalThreads) stim_segment_win(StimDev S, Chun
     }
     acc_flush(C, p, t1, tc, 0, 0, 0);
   }
-  if (lane == 0) C.bump[region] = bump;
+  region_close(C, R);
 }
 
 // ------------------------------------------------------------------- K4
@@ -368,6 +401,10 @@ struct TileSmem {
   // the item's condition tables (narrow kernels): arcs[(p << (KM-1) | row) * 2 + col]
   unsigned arcs[KM <= 4 ? KM * (1 << (KM - 1)) * 2 : 1];
   unsigned offs[KM][kTile + 1];    // per pin: window w's toggles start at offs[p][w]
+  unsigned short fend[KM][kTile];  // per pin: end of window w's toggles after the
+                                   // interconnect filter (smem-staged tiles)
+  unsigned short icfw[kTile];      // interconnect-filtered pairs per window
+  unsigned char work[kTile];       // windows left for the event loop
   unsigned ubo[kTile + 1];         // output staging offsets: prefix of the per-window bound
   TT wlen[kTile];                  // window lengths
   unsigned cnt[kTile];             // stored toggles per window
@@ -384,47 +421,105 @@ struct TileSmem {
 //            (else fanins are read in place and outputs staged in the pool);
 //   PCT100 : pathpulse 100 % -- the threshold is the delay itself, and stored
 //            edges are never retracted, so the retraction target is a register.
+// conditional SDF delay of pin p's arc (_kernels.py:139-151): row = the other
+// pins' post-transition values, ascending, packed from bit 0
+template <typename TS, typename TT, int K>
+__device__ __forceinline__ TT pin_delay(const DesignDev &D,
+                                        const TileSmem<TS, TT, (K > 0 ? K : kMaxK)> &S,
+                                        const int *arc, int p, unsigned idx, int col) {
+  constexpr bool ARC_SMEM = K > 0 && K <= 4 && sizeof(TT) == 4;
+  constexpr int ROWS = K > 0 ? 1 << (K - 1) : 1;
+  const int row = (int)((idx & ((1u << p) - 1u)) | ((idx >> (p + 1)) << p));
+  if constexpr (ARC_SMEM) return (TT)S.arcs[((p * ROWS) + row) * 2 + col];
+  else return arc_delay<TT>(D, arc[p] + row, col);
+}
+
+// per-window results of arena runs: counters (count pass) and the region of
+// the reference arena layout (store pass, waveform.py:340-345)
+template <int MODE, typename TS, typename OUT>
+__device__ __forceinline__ void record_arena(const ChunkDev &C, int g, int wr, int cnt, int peak,
+                                             int filt, int icf, int disc, unsigned y0,
+                                             OUT out_at) {
+  if (MODE & MODE_COUNTERS) {
+    const size_t gw = (size_t)g * C.Wpad + wr;
+    C.a_cnt[gw] = cnt;
+    C.a_peak[gw] = peak;
+    C.a_filt[gw] = filt;
+    C.a_icf[gw] = icf;
+    C.a_disc[gw] = disc;
+    C.a_init[gw] = (unsigned char)y0;
+  }
+  if ((MODE & MODE_STORE) == MODE_STORE) {
+    const long long o = C.a_off[(size_t)g * C.Wpad + wr];
+    const long long b_lo = C.bnd[C.w0 + wr];
+    if (o >= 0 && o + peak <= C.a_nbuf) {
+      for (int j = 0; j < peak; ++j) C.a_buf[o + j] = (long long)out_at(j) + b_lo;
+    } else if (peak) {
+      atomicExch(C.err + ERR_CAP, 1);
+    }
+  }
+}
+
 template <typename TS, typename TT, int MODE, int K, bool PCT100, bool SMEM>
 __device__ __forceinline__ void event_loop(
     const DesignDev &D, const ChunkDev &C, int g, int kk, unsigned long long lut, const TT *ic,
     const int *arc, int pct, TileSmem<TS, TT, (K > 0 ? K : kMaxK)> &S,
-    const typename std::conditional<SMEM, unsigned, const TS *>::type *inb, TS *stage, bool ok,
-    int base_w, int nact, long long &acc_tc, long long &acc_filt, long long &acc_icf,
-    long long &acc_disc) {
+    const typename std::conditional<SMEM, unsigned, const TS *>::type *inb, TS *stage,
+    unsigned stage_off, bool ok, int base_w, int nwork, long long &acc_tc, long long &acc_filt,
+    long long &acc_icf, long long &acc_disc) {
   constexpr int KM = K > 0 ? K : kMaxK;
-  constexpr bool ARC_SMEM = K > 0 && K <= 4 && sizeof(TT) == 4;
-  constexpr int ROWS = K > 0 ? 1 << (K - 1) : 1;
   const TT INF = TimeTraits<TT>::inf();
   unsigned l_tc = 0, l_filt = 0, l_icf = 0, l_disc = 0;
   int w = -1;
   bool has = false, more = ok;
-  unsigned cur[KM], end[KM], need = 0, idx = 0, y = 0, y0 = 0, so = 0;
-  TT nxt[KM], wlen = 0, t_last = 0, t_stored = 0;
+  unsigned cur[KM] = {}, end[KM] = {}, idx = 0, y = 0, y0 = 0, so = 0;
+  TT nxt[KM] = {}, wlen = 0, t_last = 0, t_stored = 0;
   int cnt = 0, peak = 0, filt = 0, icf = 0, disc = 0, cap = 0;
   bool has_last = false, last_stored = false;
   auto in_at = [&](int p, unsigned q) -> TT {
     if constexpr (SMEM) return (TT)S.slab[inb[p] + q];
     else return (TT)__ldg(inb[p] + q);
   };
+  auto out_at = [&](int i) -> TS & {
+    if constexpr (SMEM) return S.slab[stage_off + so + i];
+    else return stage[so + i];
+  };
+  // next surviving transition of pin p at or after cur[p]: with smem staging
+  // the interconnect pair filter was applied in phase 1; reading in place it
+  // runs here, lazily, exactly as sim_span does (_kernels.py:96-117)
+  auto refresh = [&](int p) {
+    unsigned q = cur[p];
+    if constexpr (!SMEM) {
+      const TT d = ic[p];
+      if (d > 0) {
+        while (q + 1 < end[p] && in_at(p, q + 1) - in_at(p, q) < d) {
+          q += 2;
+          ++icf;
+        }
+      }
+      cur[p] = q;
+    }
+    nxt[p] = q < end[p] ? in_at(p, q) + ic[p] : INF;
+  };
   while (true) {
     if (!has && more) {
       const unsigned nw = atomicAdd(&S.next, 1u);
-      if (nw < (unsigned)nact) {
-        w = (int)nw;
+      if (nw < (unsigned)nwork) {
+        w = SMEM ? (int)S.work[nw] : (int)nw;
         has = true;
+        cnt = peak = filt = disc = 0;
+        icf = SMEM ? (int)S.icfw[w] : 0;
 #pragma unroll
         for (int p = 0; p < kk; ++p) {
           cur[p] = S.offs[p][w];
-          end[p] = S.offs[p][w + 1];
-          nxt[p] = INF;
+          end[p] = SMEM ? (unsigned)S.fend[p][w] : S.offs[p][w + 1];
+          refresh(p);
         }
         idx = S.idx0[w];
         y0 = y = lut_bit(lut, kk, D.lut_words, idx);
         wlen = S.wlen[w];
         so = S.ubo[w];
         cap = (int)(S.ubo[w + 1] - so);  // peak <= #events <= fanin toggles
-        need = (1u << kk) - 1u;
-        cnt = peak = filt = icf = disc = 0;
         has_last = last_stored = false;
       } else {
         more = false;
@@ -432,29 +527,13 @@ __device__ __forceinline__ void event_loop(
     }
     if (!__any_sync(0xffffffffu, has)) break;
     if (!has) continue;
-    TT tmin = INF;
+    TT tmin = nxt[0];
 #pragma unroll
-    for (int p = 0; p < kk; ++p) {
-      if ((need >> p) & 1u) {
-        // interconnect inertial filter: drop adjacent pairs narrower than d
-        const TT d = ic[p];
-        unsigned q = cur[p];
-        if (d > 0) {
-          while (q + 1 < end[p] && in_at(p, q + 1) - in_at(p, q) < d) {
-            q += 2;
-            ++icf;
-          }
-        }
-        cur[p] = q;
-        nxt[p] = q < end[p] ? in_at(p, q) + d : INF;
-      }
-      tmin = min(tmin, nxt[p]);
-    }
-    TS *st = stage + so;
+    for (int p = 1; p < kk; ++p) tmin = min(tmin, nxt[p]);
     if (tmin == INF) {
       // window exhausted: flush the pending edge, record the window
       if (has_last && last_stored) {
-        if (cnt < cap) st[cnt] = (TS)t_last; else atomicExch(C.err + ERR_CAP, 1);
+        if (cnt < cap) out_at(cnt) = (TS)t_last; else atomicExch(C.err + ERR_CAP, 1);
         ++cnt;
         peak = max(peak, cnt);
       }
@@ -464,55 +543,32 @@ __device__ __forceinline__ void event_loop(
       l_filt += filt;
       l_icf += icf;
       l_disc += disc;
-      const int wr = base_w + w;
-      if (MODE & MODE_COUNTERS) {
-        const size_t gw = (size_t)g * C.Wpad + wr;
-        C.a_cnt[gw] = cnt;
-        C.a_peak[gw] = peak;
-        C.a_filt[gw] = filt;
-        C.a_icf[gw] = icf;
-        C.a_disc[gw] = disc;
-        C.a_init[gw] = (unsigned char)y0;
-      }
-      if ((MODE & MODE_STORE) == MODE_STORE) {
-        // store pass: the (g, w) region of the reference arena layout gets
-        // every slot the lane ever wrote, [0, peak) (waveform.py:340-345)
-        const long long o = C.a_off[(size_t)g * C.Wpad + wr];
-        const long long b_lo = C.bnd[C.w0 + wr];
-        if (o >= 0 && o + peak <= C.a_nbuf) {
-          for (int j = 0; j < peak; ++j) C.a_buf[o + j] = (long long)st[j] + b_lo;
-        } else if (peak) {
-          atomicExch(C.err + ERR_CAP, 1);
-        }
-      }
+      record_arena<MODE, TS>(C, g, base_w + w, cnt, peak, filt, icf, disc, y0,
+                             [&](int j) { return out_at(j); });
       has = false;
       continue;
     }
-    // multiple simultaneous inputs: consume every pin arriving at tmin
+    // multiple simultaneous inputs: consume every pin arriving at tmin, then
+    // advance those pins to their next transition
     unsigned sw = 0;
 #pragma unroll
-    for (int p = 0; p < kk; ++p) {
-      const bool hit = nxt[p] == tmin;
-      cur[p] += hit ? 1u : 0u;
-      sw |= (hit ? 1u : 0u) << p;
-    }
+    for (int p = 0; p < kk; ++p) sw |= (nxt[p] == tmin ? 1u : 0u) << p;
     idx ^= sw;
-    need = sw;
+#pragma unroll
+    for (int p = 0; p < kk; ++p) {
+      if ((sw >> p) & 1u) {
+        cur[p] += 1;
+        refresh(p);
+      }
+    }
     const unsigned ny = lut_bit(lut, kk, D.lut_words, idx);
     if (ny != y) {
       // conditional SDF: max over switching arcs, rows from the post state
       const int col = ny ? 0 : 1;
       TT dly = 0;
 #pragma unroll
-      for (int p = 0; p < kk; ++p) {
-        if ((sw >> p) & 1u) {
-          const int row = (int)((idx & ((1u << p) - 1u)) | ((idx >> (p + 1)) << p));
-          if constexpr (ARC_SMEM)
-            dly = max(dly, (TT)S.arcs[((p * ROWS) + row) * 2 + col]);
-          else
-            dly = max(dly, arc_delay<TT>(D, arc[p] + row, col));
-        }
-      }
+      for (int p = 0; p < kk; ++p)
+        if ((sw >> p) & 1u) dly = max(dly, pin_delay<TS, TT, K>(D, S, arc, p, idx, col));
       const TT t_out = tmin + dly;
       const TT thr = PCT100 ? dly : (TT)((unsigned long long)dly * (unsigned)pct / 100u);
       const bool have = has_last || cnt > 0;
@@ -520,18 +576,18 @@ __device__ __forceinline__ void event_loop(
       if (have && (t_out <= tgt || t_out - tgt < thr)) {
         // inertial rejection: the pulse is cancelled in full
         if (has_last) {
-          if (!last_stored) --disc;
+          disc -= last_stored ? 0 : 1;
           has_last = false;
         } else {
           // pops a stored edge (only below 100 %); its predecessor becomes
           // the retraction target
           --cnt;
-          if (!PCT100 && cnt > 0) t_stored = (TT)st[cnt - 1];
+          if (!PCT100 && cnt > 0) t_stored = (TT)out_at(cnt - 1);
         }
         ++filt;
       } else {
         if (has_last && last_stored) {
-          if (cnt < cap) st[cnt] = (TS)t_last; else atomicExch(C.err + ERR_CAP, 1);
+          if (cnt < cap) out_at(cnt) = (TS)t_last; else atomicExch(C.err + ERR_CAP, 1);
           t_stored = t_last;
           ++cnt;
           peak = max(peak, cnt);
@@ -554,8 +610,7 @@ template <typename TS, typename TT, int MODE, int K, bool PCT100>
 __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C, int g, int k,
                                           unsigned long long lut, const int *net,
                                           const TT *ic, const int *arc, int t, int pct,
-                                          TileSmem<TS, TT, (K > 0 ? K : kMaxK)> &S,
-                                          unsigned long long &bump, unsigned long long region,
+                                          TileSmem<TS, TT, (K > 0 ? K : kMaxK)> &S, Region &R,
                                           long long &acc_t1, long long &acc_tc,
                                           long long &acc_filt, long long &acc_icf,
                                           long long &acc_disc) {
@@ -612,6 +667,7 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   // slab when 2 * UB fits; otherwise inputs are read in place and outputs go
   // to this warp's region of the pool.
   const bool in_smem = 2 * UB <= (unsigned)kSlab;
+  unsigned nwork = (unsigned)nact;  // windows for the event loop
   unsigned inb_off[KM];            // smem: pin p's tile segment starts at slab[inb_off[p]]
   const TS *inb_glob[KM];          // else: read in place
   TS *stage;
@@ -626,10 +682,91 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
       o += tot[p];
     }
     stage = S.slab + UB;
+    __syncwarp();
+    // interconnect inertial filter, applied once per (pin, window): greedy
+    // removal of adjacent pairs narrower than the pin's delay, compacting the
+    // staged copy in place.  Same decisions as sim_span's lazy check
+    // (_kernels.py:96-117): each one depends only on s[q], s[q+1] and the
+    // positions are visited in the same order.
+    unsigned f[kWPL] = {0, 0, 0, 0};
+#pragma unroll
+    for (int p = 0; p < kk; ++p) {
+      const TT d = ic[p];
+#pragma unroll
+      for (int j = 0; j < kWPL; ++j) {
+        const unsigned a = inb_off[p] + S.offs[p][wl + j];
+        const unsigned b = inb_off[p] + S.offs[p][wl + j + 1];
+        unsigned e = b;
+        if (d > 0) {
+          unsigned i = a, o2 = a;
+          while (i < b) {
+            if (i + 1 < b && (TT)S.slab[i + 1] - (TT)S.slab[i] < d) {
+              i += 2;
+              ++f[j];
+            } else {
+              S.slab[o2++] = S.slab[i++];
+            }
+          }
+          e = o2;
+        }
+        S.fend[p][wl + j] = (unsigned short)(e - inb_off[p]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kWPL; ++j) S.icfw[wl + j] = (unsigned short)f[j];
+    __syncwarp();
+    // Windows left with at most one input transition need no event loop: with
+    // no earlier output edge there is nothing to retract, so the window
+    // holds exactly one output edge (t + ic + arc delay) if the function
+    // changes and the edge lands inside the window, else none.  The others go
+    // to the work list of the event loop.
+    unsigned trivial = 0;
+#pragma unroll
+    for (int j = 0; j < kWPL; ++j) {
+      const int w = wl + j;
+      if (w >= nact) continue;
+      unsigned nt = 0, pin = 0, at = 0;
+#pragma unroll
+      for (int p = 0; p < kk; ++p) {
+        const unsigned a = S.offs[p][w], e = S.fend[p][w];
+        if (e > a) { pin = (unsigned)p; at = inb_off[p] + a; }
+        nt += e - a;
+      }
+      if (nt > 1) continue;
+      trivial |= 1u << j;
+      const unsigned idx = S.idx0[w];
+      const unsigned y0 = lut_bit(lut, kk, D.lut_words, idx);
+      int cnt = 0, disc = 0;
+      TS *st = S.slab + UB + S.ubo[w];
+      if (nt == 1) {
+        const unsigned idx1 = idx ^ (1u << pin);
+        const unsigned y1 = lut_bit(lut, kk, D.lut_words, idx1);
+        if (y1 != y0) {
+          const TT t_out = (TT)S.slab[at] + ic[pin] +
+                           pin_delay<TS, TT, K>(D, S, arc, (int)pin, idx1, y1 ? 0 : 1);
+          if (t_out < S.wlen[w]) { st[0] = (TS)t_out; cnt = 1; } else { disc = 1; }
+        }
+      }
+      S.cnt[w] = (unsigned)cnt;
+      S.y0[w] = (unsigned char)y0;
+      acc_tc += cnt;
+      acc_disc += disc;
+      acc_icf += S.icfw[w];
+      record_arena<MODE, TS>(C, g, base_w + w, cnt, cnt, 0, (int)S.icfw[w], disc, y0,
+                             [&](int q) { return st[q]; });
+    }
+    // compact the remaining windows into the work list
+    unsigned m = 0;
+#pragma unroll
+    for (int j = 0; j < kWPL; ++j) m += (wl + j < nact && !((trivial >> j) & 1u)) ? 1u : 0u;
+    unsigned mx = warp_excl_scan(m, &nwork);
+#pragma unroll
+    for (int j = 0; j < kWPL; ++j)
+      if (wl + j < nact && !((trivial >> j) & 1u)) S.work[mx++] = (unsigned char)(wl + j);
   } else {
 #pragma unroll
     for (int p = 0; p < kk; ++p) inb_glob[p] = data + tb[p];
-    const unsigned long long sb = region_alloc(C, bump, region, UB);
+    const unsigned long long sb = region_alloc(C, R, UB);
     ok = sb != ~0ull;
     stage = data + (ok ? sb : 0ull);
     if (!ok) {  // pool full: the chunk is re-run; record empty windows meanwhile
@@ -642,12 +779,12 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   // ---- phase 2: one lockstep loop (see event_loop)
   if (in_smem) {
     event_loop<TS, TT, MODE, K, PCT100, true>(D, C, g, kk, lut, ic, arc, pct, S, inb_off, stage,
-                                              ok, base_w, nact, acc_tc, acc_filt, acc_icf,
-                                              acc_disc);
+                                              UB, ok, base_w, (int)nwork, acc_tc, acc_filt,
+                                              acc_icf, acc_disc);
   } else {
     event_loop<TS, TT, MODE, K, PCT100, false>(D, C, g, kk, lut, ic, arc, pct, S, inb_glob,
-                                               stage, ok, base_w, nact, acc_tc, acc_filt,
-                                               acc_icf, acc_disc);
+                                               stage, 0, ok, base_w, (int)nwork, acc_tc,
+                                               acc_filt, acc_icf, acc_disc);
   }
   __syncwarp();
 
@@ -663,7 +800,7 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   }
   unsigned CNT;
   const unsigned cx = warp_excl_scan(s, &CNT);
-  const unsigned long long ob = CNT ? region_alloc(C, bump, region, CNT) : 0ull;
+  const unsigned long long ob = CNT ? region_alloc(C, R, CNT) : 0ull;
   const bool wrote = ob != ~0ull;  // else the chunk is re-run; keep readers in bounds
   const int gnet = D.P + g;
   if (lane == 0) C.tbase[(size_t)gnet * C.Tc + t] = wrote ? ob : 0ull;
@@ -697,15 +834,15 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
 // the next item (gate, group of tpi tiles) from a per-launch counter and owns
 // a private output region (no CTA barrier, no global atomics on the data path).
 template <typename TS, typename TT, int MODE, int K, bool PCT100>
-__global__ void __launch_bounds__(kEvalThreads, 6) gate_eval(DesignDev D, ChunkDev C, LevelArgs A) {
+__global__ void __launch_bounds__(kEvalThreads, (K == 0 ? 4 : K >= 3 ? 5 : 6))
+gate_eval(DesignDev D, ChunkDev C, LevelArgs A) {
   constexpr int KM = K > 0 ? K : kMaxK;
   using SM = TileSmem<TS, TT, KM>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x / kWarp;
   SM &S = reinterpret_cast<SM *>(smem_raw)[warp];
   const unsigned lane = lane_id();
-  const unsigned long long region = (unsigned long long)blockIdx.x * kEvalWarps + warp;
-  unsigned long long bump = C.bump[region];
+  Region R = region_open(C, (unsigned long long)blockIdx.x * kEvalWarps + warp);
   const unsigned items = (unsigned)A.n * (unsigned)A.ntg;
   while (true) {
     unsigned it = 0;
@@ -739,11 +876,11 @@ __global__ void __launch_bounds__(kEvalThreads, 6) gate_eval(DesignDev D, ChunkD
     }
     long long t1 = 0, tc = 0, filt = 0, icf = 0, disc = 0;
     for (int t = t_lo; t < t_hi; ++t)
-      eval_tile<TS, TT, MODE, K, PCT100>(D, C, g, k, lut, net, ic, arc, t, A.pct, S, bump,
-                                         region, t1, tc, filt, icf, disc);
+      eval_tile<TS, TT, MODE, K, PCT100>(D, C, g, k, lut, net, ic, arc, t, A.pct, S, R, t1, tc,
+                                         filt, icf, disc);
     acc_flush(C, D.P + g, t1, tc, filt, icf, disc);
   }
-  if (lane == 0) C.bump[region] = bump;
+  region_close(C, R);
 }
 
 template <typename TS, typename TT, int K>
