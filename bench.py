@@ -254,17 +254,23 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        x0.record(stream)
+        e2e_steps = []
         for _ in range(args.e2e_steps):
-            s2 = _native.Stimulus(dev, hstim)
+            x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            x0.record(stream)
+            h0 = time.perf_counter()
+            s2 = _native.Stimulus(dev, hstim)          # H2D of this step's stimulus
+            h1 = time.perf_counter()
             step(s2)
-            host_acc.copy_(acc, non_blocking=True)
+            host_acc.copy_(acc, non_blocking=True)     # D2H of the per-net sums
+            x1.record(stream)
             stream.synchronize()
+            h2 = time.perf_counter()
             del s2
-        x1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = x0.elapsed_time(x1) / args.e2e_steps
+            e2e_steps.append((x0.elapsed_time(x1), 1e3 * (h1 - h0), 1e3 * (h2 - h1)))
+        e2e_ms = statistics.median(x[0] for x in e2e_steps)
+        e2e_upload_ms = statistics.median(x[1] for x in e2e_steps)
+        e2e_run_ms = statistics.median(x[2] for x in e2e_steps)
 
     # max over ranks
     tm = torch.tensor([ms, e2e_ms, eval_ms], dtype=torch.float64, device="cuda")
@@ -323,7 +329,9 @@ def main():
                              "k4_launches_per_step": timing["gate_eval_launches"],
                              "bytes_per_gate_window": bytes_step / (cfg.gates * Wr)},
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                        "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                        "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                        "steps": args.e2e_steps, "stat": "median per-step",
+                        "host_ms_stim_upload": e2e_upload_ms, "host_ms_run": e2e_run_ms},
                 "clocks": clocks, "gpu_launches": launches,
                 "activity": {"input_toggles_per_gw": in_tog / (cfg.gates * Wr),
                              "output_toggles_per_gw": out_tog / (cfg.gates * Wr),
