@@ -475,7 +475,7 @@ __device__ __forceinline__ void event_loop(
   unsigned cur[KM] = {}, end[KM] = {}, idx = 0, y = 0, y0 = 0, so = 0;
   TT nxt[KM] = {}, wlen = 0, t_last = 0, t_stored = 0;
   int cnt = 0, peak = 0, filt = 0, icf = 0, disc = 0, cap = 0;
-  bool has_last = false, last_stored = false;
+  bool has_last = false, last_stored = false, ovf = false;
   auto in_at = [&](int p, unsigned q) -> TT {
     if constexpr (SMEM) return (TT)S.slab[inb[p] + q];
     else return (TT)__ldg(inb[p] + q);
@@ -556,50 +556,57 @@ __device__ __forceinline__ void event_loop(
     idx ^= sw;
 #pragma unroll
     for (int p = 0; p < kk; ++p) {
-      if ((sw >> p) & 1u) {
+      const bool hit = (sw >> p) & 1u;
+      if constexpr (SMEM) {
+        // branch-free: the staged segment is in bounds of the slab even when
+        // exhausted, so the load is unconditional and the result selected
+        cur[p] += hit ? 1u : 0u;
+        const TT v = in_at(p, cur[p]) + ic[p];
+        nxt[p] = hit ? (cur[p] < end[p] ? v : INF) : nxt[p];
+      } else if (hit) {
         cur[p] += 1;
         refresh(p);
       }
     }
+    // Output side (K:136-193), as selects rather than branches so the lanes
+    // of the warp stay converged: schedule the edge through the inertial
+    // filter; cancel the pulse, or keep the previous edge and make this one
+    // the pending edge (discarded when it lands at or past the window end).
     const unsigned ny = lut_bit(lut, kk, D.lut_words, idx);
-    if (ny != y) {
-      // conditional SDF: max over switching arcs, rows from the post state
-      const int col = ny ? 0 : 1;
-      TT dly = 0;
+    const bool chg = ny != y;
+    const int col = ny ? 0 : 1;
+    TT dly = 0;
 #pragma unroll
-      for (int p = 0; p < kk; ++p)
-        if ((sw >> p) & 1u) dly = max(dly, pin_delay<TS, TT, K>(D, S, arc, p, idx, col));
-      const TT t_out = tmin + dly;
-      const TT thr = PCT100 ? dly : (TT)((unsigned long long)dly * (unsigned)pct / 100u);
-      const bool have = has_last || cnt > 0;
-      const TT tgt = has_last ? t_last : t_stored;
-      if (have && (t_out <= tgt || t_out - tgt < thr)) {
-        // inertial rejection: the pulse is cancelled in full
-        if (has_last) {
-          disc -= last_stored ? 0 : 1;
-          has_last = false;
-        } else {
-          // pops a stored edge (only below 100 %); its predecessor becomes
-          // the retraction target
-          --cnt;
-          if (!PCT100 && cnt > 0) t_stored = (TT)out_at(cnt - 1);
-        }
-        ++filt;
-      } else {
-        if (has_last && last_stored) {
-          if (cnt < cap) out_at(cnt) = (TS)t_last; else atomicExch(C.err + ERR_CAP, 1);
-          t_stored = t_last;
-          ++cnt;
-          peak = max(peak, cnt);
-        }
-        last_stored = t_out < wlen;  // else: lands at or past the window end
-        disc += last_stored ? 0 : 1;
-        has_last = true;
-        t_last = t_out;
-      }
-      y = ny;
-    }
+    for (int p = 0; p < kk; ++p)
+      if ((sw >> p) & 1u) dly = max(dly, pin_delay<TS, TT, K>(D, S, arc, p, idx, col));
+    const TT t_out = tmin + dly;
+    const TT thr = PCT100 ? dly : (TT)((unsigned long long)dly * (unsigned)pct / 100u);
+    const bool have = has_last || cnt > 0;
+    const TT tgt = has_last ? t_last : t_stored;
+    const bool cancel = chg && have && (t_out <= tgt || t_out - tgt < thr);
+    const bool emit = chg && !cancel;
+    // cancellation: drop the pending edge, or (below 100 %) pop a stored one
+    // whose predecessor becomes the retraction target
+    const bool pop = cancel && !has_last;
+    disc -= (cancel && has_last && !last_stored) ? 1 : 0;
+    cnt -= pop ? 1 : 0;
+    if (!PCT100 && pop && cnt > 0) t_stored = (TT)out_at(cnt - 1);
+    filt += cancel ? 1 : 0;
+    // emission: the previous pending edge (if it landed in the window) is stored
+    const bool store = emit && has_last && last_stored;
+    if (store && cnt < cap) out_at(cnt) = (TS)t_last;
+    ovf |= store && cnt >= cap;
+    t_stored = store ? t_last : t_stored;
+    cnt += store ? 1 : 0;
+    peak = max(peak, cnt);
+    const bool inwin = t_out < wlen;
+    disc += (emit && !inwin) ? 1 : 0;
+    last_stored = emit ? inwin : last_stored;
+    t_last = emit ? t_out : t_last;
+    has_last = emit || (has_last && !cancel);
+    y = chg ? ny : y;
   }
+  if (ovf) atomicExch(C.err + ERR_CAP, 1);
   acc_tc += l_tc;
   acc_filt += l_filt;
   acc_icf += l_icf;
