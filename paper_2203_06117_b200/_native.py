@@ -16,7 +16,7 @@ from .errors import CapacityError, ConsistencyError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_NAME = "libglsim_cuda.so"
-LIB_PATH = os.path.join(_HERE, LIB_NAME)
+LIB_PATH = os.path.join(_HERE, os.environ.get("GLSIM_LIB", LIB_NAME))
 
 GS_OK, GS_ERR_ARG, GS_ERR_CUDA, GS_ERR_NODEVICE, GS_ERR_CAPACITY, GS_ERR_CONSISTENCY = range(6)
 

@@ -36,10 +36,14 @@
 #include <cuda_runtime.h>
 #include <type_traits>
 
+#ifndef GS_TILE
+#define GS_TILE 128
+#endif
+
 namespace gs {
 
 constexpr int kWarp = 32;
-constexpr int kTile = 128;                  // windows per (gate, tile) work unit
+constexpr int kTile = GS_TILE;              // windows per (gate, tile) work unit
 constexpr int kWPL = kTile / kWarp;         // windows per lane in the cooperative phases
 constexpr int kEvalWarps = 4;               // warps per K4 CTA
 constexpr int kEvalThreads = kEvalWarps * kWarp;
@@ -217,19 +221,41 @@ __device__ __forceinline__ void acc_flush(const ChunkDev &C, int net, long long 
   }
 }
 
-// window-start bits of the lane's 4 windows (nibble) -> the tile's 32-bit
-// words; lanes with (lane & 7) == 0 write word lane >> 3
-__device__ __forceinline__ void store_init_words(unsigned *row, int tile, unsigned nib) {
+// window-start bits of the lane's kWPL windows -> the tile's 32-bit words
+// (32 / kWPL lanes per word; the first lane of each group writes it)
+__device__ __forceinline__ void store_init_words(unsigned *row, int tile, unsigned bits) {
+  constexpr int LPW = 32 / kWPL;  // lanes per word
   const unsigned lane = lane_id();
-  unsigned w = nib << ((lane & 7) * kWPL);
-  w |= __shfl_xor_sync(0xffffffffu, w, 1);
-  w |= __shfl_xor_sync(0xffffffffu, w, 2);
-  w |= __shfl_xor_sync(0xffffffffu, w, 4);
-  if ((lane & 7) == 0) row[tile * (kTile / 32) + (lane >> 3)] = w;
+  unsigned w = bits << ((lane % LPW) * kWPL);
+#pragma unroll
+  for (int o = 1; o < LPW; o <<= 1) w |= __shfl_xor_sync(0xffffffffu, w, o);
+  if (lane % LPW == 0) row[tile * (kTile / 32) + lane / LPW] = w;
 }
 
-__device__ __forceinline__ uint4 ldg_u4(const unsigned *p) {
-  return __ldg(reinterpret_cast<const uint4 *>(p));
+// the lane's kWPL window-start bits from a tile of init words
+__device__ __forceinline__ unsigned load_init_bits(const unsigned *row, int tile) {
+  const unsigned lane = lane_id();
+  const unsigned w = __ldg(row + tile * (kTile / 32) + (lane * kWPL) / 32);
+  return (w >> ((lane * kWPL) % 32)) & ((1u << kWPL) - 1u);
+}
+
+// the lane's kWPL consecutive window counts (16-byte vector loads / stores)
+__device__ __forceinline__ void load_counts(const unsigned *p, unsigned *c) {
+#pragma unroll
+  for (int q = 0; q < kWPL / 4; ++q) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p) + q);
+    c[4 * q] = v.x;
+    c[4 * q + 1] = v.y;
+    c[4 * q + 2] = v.z;
+    c[4 * q + 3] = v.w;
+  }
+}
+
+__device__ __forceinline__ void store_counts(unsigned *p, const unsigned *c, bool keep) {
+#pragma unroll
+  for (int q = 0; q < kWPL / 4; ++q)
+    reinterpret_cast<uint4 *>(p)[q] =
+        keep ? make_uint4(c[4 * q], c[4 * q + 1], c[4 * q + 2], c[4 * q + 3]) : make_uint4(0, 0, 0, 0);
 }
 
 // ----------------------------------------------------------------- K1 (CSR)
@@ -288,7 +314,7 @@ __global__ void __launch_bounds__(256) stim_segment_csr(StimDev S, ChunkDev C, i
           nib |= ((init ^ (unsigned)start) & 1u) << j;
         }
       }
-      *reinterpret_cast<uint4 *>(C.cnt + (size_t)p * C.Wpad + wl) = make_uint4(c[0], c[1], c[2], c[3]);
+      store_counts(C.cnt + (size_t)p * C.Wpad + wl, c, true);
       if (lane == 0) C.tbase[(size_t)p * C.Tc + t] = (unsigned long long)(off + cut0);
       store_init_words(C.init + (size_t)p * Tw, t, nib);
     }
@@ -336,8 +362,7 @@ __global__ void __launch_bounds__(kEvalThreads) stim_segment_win(StimDev S, Chun
       const unsigned long long base = total ? region_alloc(C, R, total) : 0ull;
       const bool wrote = base != ~0ull;
       if (lane == 0) C.tbase[(size_t)p * C.Tc + t] = wrote ? base : 0ull;
-      *reinterpret_cast<uint4 *>(C.cnt + (size_t)p * C.Wpad + wl) =
-          wrote ? make_uint4(c[0], c[1], c[2], c[3]) : make_uint4(0, 0, 0, 0);
+      store_counts(C.cnt + (size_t)p * C.Wpad + wl, c, wrote);
       store_init_words(C.init + (size_t)p * Tw, t, nib);
       unsigned long long o = base + ex;
 #pragma unroll
@@ -465,11 +490,16 @@ __device__ __forceinline__ void event_loop(
     const DesignDev &D, const ChunkDev &C, int g, int kk, unsigned long long lut, const TT *ic,
     const int *arc, int pct, TileSmem<TS, TT, (K > 0 ? K : kMaxK)> &S,
     const typename std::conditional<SMEM, unsigned, const TS *>::type *inb, TS *stage,
-    unsigned stage_off, bool ok, int base_w, int nwork, long long &acc_tc, long long &acc_filt,
-    long long &acc_icf, long long &acc_disc) {
+    unsigned stage_off, bool ok, int base_w, int nwork, long long &acc_t1, long long &acc_tc,
+    long long &acc_filt, long long &acc_icf, long long &acc_disc) {
   constexpr int KM = K > 0 ? K : kMaxK;
   const TT INF = TimeTraits<TT>::inf();
   unsigned l_tc = 0, l_filt = 0, l_icf = 0, l_disc = 0;
+  long long l_t1 = 0;
+  // dwell at 1 (dwell_sweep), accumulated as edges are stored; valid at 100 %
+  // where a stored edge is final (below that, phase 3 recomputes it)
+  unsigned dv = 0;
+  TT dt = 0, t1w = 0;
   int w = -1;
   bool has = false, more = ok;
   unsigned cur[KM] = {}, end[KM] = {}, idx = 0, y = 0, y0 = 0, so = 0;
@@ -521,6 +551,8 @@ __device__ __forceinline__ void event_loop(
         so = S.ubo[w];
         cap = (int)(S.ubo[w + 1] - so);  // peak <= #events <= fanin toggles
         has_last = last_stored = false;
+        dv = y0;
+        dt = t1w = 0;
       } else {
         more = false;
       }
@@ -536,7 +568,11 @@ __device__ __forceinline__ void event_loop(
         if (cnt < cap) out_at(cnt) = (TS)t_last; else atomicExch(C.err + ERR_CAP, 1);
         ++cnt;
         peak = max(peak, cnt);
+        t1w += dv ? t_last - dt : (TT)0;
+        dv ^= 1u;
+        dt = t_last;
       }
+      if (PCT100) l_t1 += (long long)(t1w + (dv ? wlen - dt : (TT)0));
       S.cnt[w] = (unsigned)cnt;
       S.y0[w] = (unsigned char)y0;
       l_tc += cnt;
@@ -599,6 +635,9 @@ __device__ __forceinline__ void event_loop(
     t_stored = store ? t_last : t_stored;
     cnt += store ? 1 : 0;
     peak = max(peak, cnt);
+    t1w += (store && dv) ? t_last - dt : (TT)0;
+    dv ^= store ? 1u : 0u;
+    dt = store ? t_last : dt;
     const bool inwin = t_out < wlen;
     disc += (emit && !inwin) ? 1 : 0;
     last_stored = emit ? inwin : last_stored;
@@ -607,6 +646,7 @@ __device__ __forceinline__ void event_loop(
     y = chg ? ny : y;
   }
   if (ovf) atomicExch(C.err + ERR_CAP, 1);
+  acc_t1 += l_t1;
   acc_tc += l_tc;
   acc_filt += l_filt;
   acc_icf += l_icf;
@@ -634,34 +674,39 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   // ---- phase 1: fanin tiles -> per-window offsets, start vectors, bounds
   unsigned long long tb[KM];
   unsigned tot[KM];
-  unsigned ub[kWPL] = {0, 0, 0, 0};
-  unsigned ix[kWPL] = {0, 0, 0, 0};
+  unsigned ub[kWPL], ix[kWPL];
+#pragma unroll
+  for (int j = 0; j < kWPL; ++j) ub[j] = ix[j] = 0;
 #pragma unroll
   for (int p = 0; p < kk; ++p) {
     const int nn = net[p];
-    const uint4 c = ldg_u4(C.cnt + (size_t)nn * C.Wpad + base_w + wl);
-    const unsigned ex = warp_excl_scan(c.x + c.y + c.z + c.w, &tot[p]);
-    S.offs[p][wl] = ex;
-    S.offs[p][wl + 1] = ex + c.x;
-    S.offs[p][wl + 2] = ex + c.x + c.y;
-    S.offs[p][wl + 3] = ex + c.x + c.y + c.z;
+    unsigned c[kWPL];
+    load_counts(C.cnt + (size_t)nn * C.Wpad + base_w + wl, c);
+    unsigned s4 = 0;
+#pragma unroll
+    for (int j = 0; j < kWPL; ++j) s4 += c[j];
+    unsigned ex = warp_excl_scan(s4, &tot[p]);
+#pragma unroll
+    for (int j = 0; j < kWPL; ++j) {
+      S.offs[p][wl + j] = ex;
+      ex += c[j];
+      ub[j] += c[j];
+    }
     if (lane == kWarp - 1) S.offs[p][kTile] = tot[p];
     tb[p] = __ldg(C.tbase + (size_t)nn * C.Tc + t);
-    const unsigned nib = (__ldg(C.init + (size_t)nn * Tw + t * (kTile / 32) + (lane >> 3)) >>
-                          ((lane & 7) * kWPL)) & 0xfu;
+    const unsigned bits = load_init_bits(C.init + (size_t)nn * Tw, t);
 #pragma unroll
-    for (int j = 0; j < kWPL; ++j) ix[j] |= ((nib >> j) & 1u) << p;
-    ub[0] += c.x;
-    ub[1] += c.y;
-    ub[2] += c.z;
-    ub[3] += c.w;
+    for (int j = 0; j < kWPL; ++j) ix[j] |= ((bits >> j) & 1u) << p;
   }
-  unsigned UB;
-  const unsigned ux = warp_excl_scan(ub[0] + ub[1] + ub[2] + ub[3], &UB);
-  S.ubo[wl] = ux;
-  S.ubo[wl + 1] = ux + ub[0];
-  S.ubo[wl + 2] = ux + ub[0] + ub[1];
-  S.ubo[wl + 3] = ux + ub[0] + ub[1] + ub[2];
+  unsigned UB, us = 0;
+#pragma unroll
+  for (int j = 0; j < kWPL; ++j) us += ub[j];
+  unsigned ux = warp_excl_scan(us, &UB);
+#pragma unroll
+  for (int j = 0; j < kWPL; ++j) {
+    S.ubo[wl + j] = ux;
+    ux += ub[j];
+  }
   if (lane == kWarp - 1) S.ubo[kTile] = UB;
 #pragma unroll
   for (int j = 0; j < kWPL; ++j) {
@@ -695,7 +740,9 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
     // staged copy in place.  Same decisions as sim_span's lazy check
     // (_kernels.py:96-117): each one depends only on s[q], s[q+1] and the
     // positions are visited in the same order.
-    unsigned f[kWPL] = {0, 0, 0, 0};
+    unsigned f[kWPL];
+#pragma unroll
+    for (int j = 0; j < kWPL; ++j) f[j] = 0;
 #pragma unroll
     for (int p = 0; p < kk; ++p) {
       const TT d = ic[p];
@@ -705,16 +752,21 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
         const unsigned b = inb_off[p] + S.offs[p][wl + j + 1];
         unsigned e = b;
         if (d > 0) {
-          unsigned i = a, o2 = a;
-          while (i < b) {
-            if (i + 1 < b && (TT)S.slab[i + 1] - (TT)S.slab[i] < d) {
-              i += 2;
-              ++f[j];
-            } else {
-              S.slab[o2++] = S.slab[i++];
+          // the prefix before the first narrow pair stays where it is
+          unsigned i = a;
+          while (i + 1 < b && (TT)S.slab[i + 1] - (TT)S.slab[i] >= d) ++i;
+          if (i + 1 < b) {
+            unsigned o2 = i;
+            while (i < b) {
+              if (i + 1 < b && (TT)S.slab[i + 1] - (TT)S.slab[i] < d) {
+                i += 2;
+                ++f[j];
+              } else {
+                S.slab[o2++] = S.slab[i++];
+              }
             }
+            e = o2;
           }
-          e = o2;
         }
         S.fend[p][wl + j] = (unsigned short)(e - inb_off[p]);
       }
@@ -752,8 +804,10 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
           const TT t_out = (TT)S.slab[at] + ic[pin] +
                            pin_delay<TS, TT, K>(D, S, arc, (int)pin, idx1, y1 ? 0 : 1);
           if (t_out < S.wlen[w]) { st[0] = (TS)t_out; cnt = 1; } else { disc = 1; }
+          if (PCT100 && cnt) acc_t1 += y0 ? (long long)t_out : (long long)(S.wlen[w] - t_out);
         }
       }
+      if (PCT100 && !cnt && y0) acc_t1 += (long long)S.wlen[w];
       S.cnt[w] = (unsigned)cnt;
       S.y0[w] = (unsigned char)y0;
       acc_tc += cnt;
@@ -786,12 +840,12 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   // ---- phase 2: one lockstep loop (see event_loop)
   if (in_smem) {
     event_loop<TS, TT, MODE, K, PCT100, true>(D, C, g, kk, lut, ic, arc, pct, S, inb_off, stage,
-                                              UB, ok, base_w, (int)nwork, acc_tc, acc_filt,
-                                              acc_icf, acc_disc);
+                                              UB, ok, base_w, (int)nwork, acc_t1, acc_tc,
+                                              acc_filt, acc_icf, acc_disc);
   } else {
     event_loop<TS, TT, MODE, K, PCT100, false>(D, C, g, kk, lut, ic, arc, pct, S, inb_glob,
-                                               stage, 0, ok, base_w, (int)nwork, acc_tc,
-                                               acc_filt, acc_icf, acc_disc);
+                                               stage, 0, ok, base_w, (int)nwork, acc_t1,
+                                               acc_tc, acc_filt, acc_icf, acc_disc);
   }
   __syncwarp();
 
@@ -811,8 +865,7 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   const bool wrote = ob != ~0ull;  // else the chunk is re-run; keep readers in bounds
   const int gnet = D.P + g;
   if (lane == 0) C.tbase[(size_t)gnet * C.Tc + t] = wrote ? ob : 0ull;
-  *reinterpret_cast<uint4 *>(C.cnt + (size_t)gnet * C.Wpad + base_w + wl) =
-      wrote ? make_uint4(c[0], c[1], c[2], c[3]) : make_uint4(0, 0, 0, 0);
+  store_counts(C.cnt + (size_t)gnet * C.Wpad + base_w + wl, c, wrote);
   store_init_words(C.init + (size_t)gnet * Tw, t, nib);
   TS *dst = data + (wrote ? ob + cx : 0ull);
   long long t1 = 0;
@@ -820,16 +873,22 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   for (int j = 0; j < kWPL; ++j) {
     if (wl + j >= nact) continue;
     const TS *src = stage + S.ubo[wl + j];
-    unsigned v = (nib >> j) & 1u;
-    long long prev = 0;
-    for (unsigned q = 0; q < c[j]; ++q) {
-      const TS x = src[q];
-      if (wrote) dst[q] = x;
-      if (v) t1 += (long long)x - prev;
-      v ^= 1u;
-      prev = (long long)x;
+    if (PCT100) {
+      // dwell already accumulated in phases 1 and 2
+      if (wrote)
+        for (unsigned q = 0; q < c[j]; ++q) dst[q] = src[q];
+    } else {
+      unsigned v = (nib >> j) & 1u;
+      long long prev = 0;
+      for (unsigned q = 0; q < c[j]; ++q) {
+        const TS x = src[q];
+        if (wrote) dst[q] = x;
+        if (v) t1 += (long long)x - prev;
+        v ^= 1u;
+        prev = (long long)x;
+      }
+      if (v) t1 += (long long)S.wlen[wl + j] - prev;
     }
-    if (v) t1 += (long long)S.wlen[wl + j] - prev;
     dst += c[j];
   }
   acc_t1 += t1;
