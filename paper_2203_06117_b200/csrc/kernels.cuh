@@ -425,6 +425,10 @@ struct TileSmem {
   TS slab[kSlab];                  // staged fanin segments, then output staging
   // the item's condition tables (narrow kernels): arcs[(p << (KM-1) | row) * 2 + col]
   unsigned arcs[KM <= 4 ? KM * (1 << (KM - 1)) * 2 : 1];
+  // output delay by (switching pins, post-transition inputs, edge): the max
+  // over the switching arcs of the conditioned delay (K:139-151), tabulated
+  // once per gate so the event step does one lookup
+  unsigned dtab[KM <= 4 ? (1 << (2 * KM)) * 2 : 1];
   unsigned offs[KM][kTile + 1];    // per pin: window w's toggles start at offs[p][w]
   unsigned short fend[KM][kTile];  // per pin: end of window w's toggles after the
                                    // interconnect filter (smem-staged tiles)
@@ -529,7 +533,8 @@ __device__ __forceinline__ void event_loop(
       }
       cur[p] = q;
     }
-    nxt[p] = q < end[p] ? in_at(p, q) + ic[p] : INF;
+    const TT add = (SMEM && sizeof(TT) == 4) ? (TT)0 : ic[p];  // staged = arrival time
+    nxt[p] = q < end[p] ? in_at(p, q) + add : INF;
   };
   while (true) {
     if (!has && more) {
@@ -597,7 +602,7 @@ __device__ __forceinline__ void event_loop(
         // branch-free: the staged segment is in bounds of the slab even when
         // exhausted, so the load is unconditional and the result selected
         cur[p] += hit ? 1u : 0u;
-        const TT v = in_at(p, cur[p]) + ic[p];
+        const TT v = in_at(p, cur[p]) + (sizeof(TT) == 4 ? (TT)0 : ic[p]);
         nxt[p] = hit ? (cur[p] < end[p] ? v : INF) : nxt[p];
       } else if (hit) {
         cur[p] += 1;
@@ -612,29 +617,44 @@ __device__ __forceinline__ void event_loop(
     const bool chg = ny != y;
     const int col = ny ? 0 : 1;
     TT dly = 0;
+    if constexpr (K > 0 && K <= 4 && sizeof(TT) == 4) {
+      dly = (TT)S.dtab[(((sw << K) | idx) << 1) | (unsigned)col];
+    } else {
 #pragma unroll
-    for (int p = 0; p < kk; ++p)
-      if ((sw >> p) & 1u) dly = max(dly, pin_delay<TS, TT, K>(D, S, arc, p, idx, col));
+      for (int p = 0; p < kk; ++p)
+        if ((sw >> p) & 1u) dly = max(dly, pin_delay<TS, TT, K>(D, S, arc, p, idx, col));
+    }
     const TT t_out = tmin + dly;
     const TT thr = PCT100 ? dly : (TT)((unsigned long long)dly * (unsigned)pct / 100u);
-    const bool have = has_last || cnt > 0;
-    const TT tgt = has_last ? t_last : t_stored;
-    const bool cancel = chg && have && (t_out <= tgt || t_out - tgt < thr);
+    bool cancel;
+    if constexpr (PCT100) {
+      // event times strictly increase, so with no pending edge the newest
+      // stored edge (stored when a later edge survived against it) is never
+      // closer than the new edge's own delay: only the pending edge can be
+      // cancelled, and stored edges are final
+      cancel = chg && has_last && (t_out <= t_last || t_out - t_last < thr);
+    } else {
+      const bool have = has_last || cnt > 0;
+      const TT tgt = has_last ? t_last : t_stored;
+      cancel = chg && have && (t_out <= tgt || t_out - tgt < thr);
+    }
     const bool emit = chg && !cancel;
     // cancellation: drop the pending edge, or (below 100 %) pop a stored one
     // whose predecessor becomes the retraction target
-    const bool pop = cancel && !has_last;
+    const bool pop = !PCT100 && cancel && !has_last;
     disc -= (cancel && has_last && !last_stored) ? 1 : 0;
-    cnt -= pop ? 1 : 0;
-    if (!PCT100 && pop && cnt > 0) t_stored = (TT)out_at(cnt - 1);
+    if (!PCT100) {
+      cnt -= pop ? 1 : 0;
+      if (pop && cnt > 0) t_stored = (TT)out_at(cnt - 1);
+    }
     filt += cancel ? 1 : 0;
     // emission: the previous pending edge (if it landed in the window) is stored
     const bool store = emit && has_last && last_stored;
     if (store && cnt < cap) out_at(cnt) = (TS)t_last;
     ovf |= store && cnt >= cap;
-    t_stored = store ? t_last : t_stored;
+    if (!PCT100) t_stored = store ? t_last : t_stored;
     cnt += store ? 1 : 0;
-    peak = max(peak, cnt);
+    if (MODE != MODE_STATS) peak = max(peak, cnt);
     t1w += (store && dv) ? t_last - dt : (TT)0;
     dv ^= store ? 1u : 0u;
     dt = store ? t_last : dt;
@@ -729,7 +749,10 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
 #pragma unroll
     for (int p = 0; p < kk; ++p) {
       const TS *src = data + tb[p];
-      for (unsigned i = lane; i < tot[p]; i += kWarp) S.slab[o + i] = __ldg(src + i);
+      // narrow kernels stage arrival times (toggle + interconnect delay); the
+      // pair filter below only compares differences, so it is unaffected
+      const TS add = sizeof(TT) == 4 ? (TS)ic[p] : (TS)0;
+      for (unsigned i = lane; i < tot[p]; i += kWarp) S.slab[o + i] = __ldg(src + i) + add;
       inb_off[p] = o;
       o += tot[p];
     }
@@ -801,7 +824,7 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
         const unsigned idx1 = idx ^ (1u << pin);
         const unsigned y1 = lut_bit(lut, kk, D.lut_words, idx1);
         if (y1 != y0) {
-          const TT t_out = (TT)S.slab[at] + ic[pin] +
+          const TT t_out = (TT)S.slab[at] + (sizeof(TT) == 4 ? (TT)0 : ic[pin]) +
                            pin_delay<TS, TT, K>(D, S, arc, (int)pin, idx1, y1 ? 0 : 1);
           if (t_out < S.wlen[w]) { st[0] = (TS)t_out; cnt = 1; } else { disc = 1; }
           if (PCT100 && cnt) acc_t1 += y0 ? (long long)t_out : (long long)(S.wlen[w] - t_out);
@@ -937,6 +960,19 @@ gate_eval(DesignDev D, ChunkDev C, LevelArgs A) {
       for (int i = (int)lane; i < (K > 0 ? K : 1) * R * 2; i += kWarp) {
         const int pp = i / (2 * R), rc = i % (2 * R);
         S.arcs[i] = __ldg(D.arc32 + (size_t)arc[pp] * 2 + rc);
+      }
+      __syncwarp();
+      constexpr int KK = K > 0 ? K : 1;
+      for (int i = (int)lane; i < (1 << (2 * KK)) * 2; i += kWarp) {
+        const unsigned col = i & 1, id = (i >> 1) & ((1u << KK) - 1), sw = (unsigned)i >> (KK + 1);
+        unsigned dmax = 0;
+        for (int pp = 0; pp < KK; ++pp) {
+          if ((sw >> pp) & 1u) {
+            const unsigned row = (id & ((1u << pp) - 1u)) | ((id >> (pp + 1)) << pp);
+            dmax = max(dmax, S.arcs[((pp * R) + row) * 2 + col]);
+          }
+        }
+        S.dtab[i] = dmax;
       }
       __syncwarp();
     }
