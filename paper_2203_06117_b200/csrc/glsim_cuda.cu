@@ -919,6 +919,16 @@ int gs_run_arena(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct,
   return GS_OK;
 }
 
+#ifdef GS_PROF
+// debug builds only (not part of the ABI header): read and clear the counters
+int gs_prof_read(unsigned long long *out16) {
+  CK(cudaMemcpyFromSymbol(out16, gs_prof_counters, sizeof(unsigned long long) * 16));
+  unsigned long long z[16] = {0};
+  CK(cudaMemcpyToSymbol(gs_prof_counters, z, sizeof(z)));
+  return GS_OK;
+}
+#endif
+
 int gs_last_timing(gs_engine *e, gs_timing *t) {
   if (!e || !t) return fail(GS_ERR_ARG, "null argument");
   *t = e->last;

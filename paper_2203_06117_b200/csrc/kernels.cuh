@@ -33,6 +33,7 @@
 #pragma once
 #include <cstdint>
 #include <climits>
+#include <cuda_pipeline.h>
 #include <cuda_runtime.h>
 #include <type_traits>
 
@@ -41,6 +42,21 @@
 #endif
 
 namespace gs {
+
+// Debug-only instrumentation (-DGS_PROF): per-phase SM clock cycles and event
+// loop efficiency counters, summed over all warps into gs_prof_counters.
+#ifdef GS_PROF
+__device__ unsigned long long gs_prof_counters[16];
+#define GS_PROF_T(v_) const long long v_ = clock64()
+#define GS_PROF_ADD(i_, n_) \
+  do { if ((threadIdx.x & 31) == 0) atomicAdd(&gs_prof_counters[i_], (unsigned long long)(n_)); } while (0)
+#else
+#define GS_PROF_T(v_)
+#define GS_PROF_ADD(i_, n_) do { } while (0)
+#endif
+enum ProfSlot { PF_PHASE1 = 0, PF_CLOSED = 1, PF_LOOP = 2, PF_PHASE3 = 3, PF_ITER = 4,
+                PF_BUSY_LANES = 5, PF_EVENTS = 6, PF_LOOP_WINDOWS = 7, PF_TILES = 8,
+                PF_TRIVIAL = 9, PF_SLOW_TILES = 10 };
 
 constexpr int kWarp = 32;
 constexpr int kTile = GS_TILE;              // windows per (gate, tile) work unit
@@ -421,7 +437,7 @@ __device__ __forceinline__ long long arc_delay<long long>(const DesignDev &D, in
 
 // per-warp shared-memory tile state
 template <typename TS, typename TT, int KM>
-struct TileSmem {
+struct alignas(16) TileSmem {
   TS slab[kSlab];                  // staged fanin segments, then output staging
   // the item's condition tables (narrow kernels): arcs[(p << (KM-1) | row) * 2 + col]
   unsigned arcs[KM <= 4 ? KM * (1 << (KM - 1)) * 2 : 1];
@@ -429,6 +445,7 @@ struct TileSmem {
   // over the switching arcs of the conditioned delay (K:139-151), tabulated
   // once per gate so the event step does one lookup
   unsigned dtab[KM <= 4 ? (1 << (2 * KM)) * 2 : 1];
+
   unsigned offs[KM][kTile + 1];    // per pin: window w's toggles start at offs[p][w]
   unsigned short fend[KM][kTile];  // per pin: end of window w's toggles after the
                                    // interconnect filter (smem-staged tiles)
@@ -563,6 +580,13 @@ __device__ __forceinline__ void event_loop(
       }
     }
     if (!__any_sync(0xffffffffu, has)) break;
+#ifdef GS_PROF
+    {
+      const unsigned b = __ballot_sync(0xffffffffu, has);
+      GS_PROF_ADD(PF_ITER, 1);
+      GS_PROF_ADD(PF_BUSY_LANES, __popc(b));
+    }
+#endif
     if (!has) continue;
     TT tmin = nxt[0];
 #pragma unroll
@@ -691,6 +715,11 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   const int Tw = C.Wpad / 32;
   TS *data = reinterpret_cast<TS *>(C.data);
 
+  GS_PROF_T(pt0);
+#ifdef GS_PROF
+  long long pt1 = 0;
+#endif
+  GS_PROF_ADD(PF_TILES, 1);
   // ---- phase 1: fanin tiles -> per-window offsets, start vectors, bounds
   unsigned long long tb[KM];
   unsigned tot[KM];
@@ -746,15 +775,23 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   bool ok = true;
   if (in_smem) {
     unsigned o = 0;
+    // all pins' segments in flight at once (cp.async), one wait
 #pragma unroll
     for (int p = 0; p < kk; ++p) {
       const TS *src = data + tb[p];
-      // narrow kernels stage arrival times (toggle + interconnect delay); the
-      // pair filter below only compares differences, so it is unaffected
-      const TS add = sizeof(TT) == 4 ? (TS)ic[p] : (TS)0;
-      for (unsigned i = lane; i < tot[p]; i += kWarp) S.slab[o + i] = __ldg(src + i) + add;
+      for (unsigned i = lane; i < tot[p]; i += kWarp)
+        __pipeline_memcpy_async(&S.slab[o + i], src + i, sizeof(TS));
       inb_off[p] = o;
       o += tot[p];
+    }
+    __pipeline_commit();
+    __pipeline_wait_prior(0);
+    if constexpr (sizeof(TT) == 4) {
+      // narrow kernels stage arrival times (toggle + interconnect delay); the
+      // pair filter below only compares differences, so it is unaffected
+#pragma unroll
+      for (int p = 0; p < kk; ++p)
+        for (unsigned i = lane; i < tot[p]; i += kWarp) S.slab[inb_off[p] + i] += (TS)ic[p];
     }
     stage = S.slab + UB;
     __syncwarp();
@@ -797,6 +834,10 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
 #pragma unroll
     for (int j = 0; j < kWPL; ++j) S.icfw[wl + j] = (unsigned short)f[j];
     __syncwarp();
+#ifdef GS_PROF
+    pt1 = clock64();
+    GS_PROF_ADD(PF_PHASE1, pt1 - pt0);
+#endif
     // Windows left with at most one input transition need no event loop: with
     // no earlier output edge there is nothing to retract, so the window
     // holds exactly one output edge (t + ic + arc delay) if the function
@@ -860,6 +901,17 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   }
   __syncwarp();
 
+  GS_PROF_T(pt2);
+#ifdef GS_PROF
+  if (in_smem) {
+    GS_PROF_ADD(PF_CLOSED, pt2 - pt1);
+    GS_PROF_ADD(PF_TRIVIAL, nact - (int)nwork);
+  } else {
+    GS_PROF_ADD(PF_PHASE1, pt2 - pt0);
+    GS_PROF_ADD(PF_SLOW_TILES, 1);
+  }
+  GS_PROF_ADD(PF_LOOP_WINDOWS, nwork);
+#endif
   // ---- phase 2: one lockstep loop (see event_loop)
   if (in_smem) {
     event_loop<TS, TT, MODE, K, PCT100, true>(D, C, g, kk, lut, ic, arc, pct, S, inb_off, stage,
@@ -872,6 +924,8 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   }
   __syncwarp();
 
+  GS_PROF_T(pt3);
+  GS_PROF_ADD(PF_LOOP, pt3 - pt2);
   // ---- phase 3: compaction (warp scan of the lane's 4 windows' counts);
   // the copy out of the staging area also yields the dwell at 1 (dwell_sweep)
   unsigned c[kWPL], nib = 0, s = 0;
@@ -916,6 +970,8 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   }
   acc_t1 += t1;
   __syncwarp();
+  GS_PROF_T(pt4);
+  GS_PROF_ADD(PF_PHASE3, pt4 - pt3);
 }
 
 // One launch per (logic level, fanin-count group); the level barrier is the
