@@ -215,3 +215,42 @@ def test_c_abi_init_values_matches_oracle(oracle_lib):
     st = oracle_lib.Stimulus(gen.oracle_inputs(nl, waves), b)
     assert np.array_equal(vals, oracle_lib.init_values(d, st))
     assert np.array_equal(vals[nl.num_pis:], ref["initials"])
+
+
+def test_config_c1_ripple_carry_adder_matches_oracle(oracle_lib):
+    # 20-bit ripple-carry adder, 1k windows, full SDF (COND +
+    # INTERCONNECT), documents through the text front-ends
+    from paper_2203_06117_b200 import synth
+    lib_t, net_t, sdf_t, vcd_t, period = synth.rca_docs()
+    docs = gen.Docs(lib_t, net_t, sdf_t, vcd_t, period)
+    nl, lv, delays, stim, arena, diag, stats = gpu_run(docs)
+    assert nl.num_gates == 100 and stim.num_windows == 1000
+    waves = gen.load(docs, api)[3]
+    d, st, oa, os_ = oracle_lib.simulate(lv, delays, gen.oracle_inputs(nl, waves),
+                                         stim.boundaries, threads=4)
+    for f in ("buf", "offsets", "caps", "counts", "initials", "filtered", "ic_filtered",
+              "discarded"):
+        assert np.array_equal(getattr(arena, f), oa[f]), f
+    for f in ("t0", "t1", "tc", "ig"):
+        assert np.array_equal(getattr(stats, f), os_[f]), f
+    assert int(stats.tc.sum()) > 0
+
+
+@pytest.mark.parametrize("variant", ["C5", "C5-pct0", "C5-avg", "C5-avg-pct0"])
+def test_config_c5_variants_match_oracle(oracle_lib, variant):
+    # SURVEY §8(d) C5 feature ablation on the C3 netlist family (full/averaged
+    # SDF x pathpulse 100/0), checked on a scaled-down design and 64 windows
+    from paper_2203_06117_b200 import synth
+    cfg = synth.config(variant, gates=20_000, levels=25, ppis=2_000, pis=100, windows=64)
+    m = synth.design(cfg)
+    stim = synth.stimulus(cfg, 0, 64)
+    stats, diag = api.simulate_streaming(m, stim, api.RunConfig(pathpulse_pct=cfg.pct))
+    d = oracle_lib.Design.from_arrays(m.num_pis, m.order, m.level_starts, m.pin_off, m.pin_net,
+                                      m.pin_ic, m.pin_arc, m.arc_rows, m.lut_off, m.lut_bits)
+    st = oracle_lib.Stimulus.from_csr(stim.pi_off, stim.pi_times, stim.pi_init, stim.boundaries)
+    a = oracle_lib.two_pass_simulate(d, st, pct=cfg.pct, threads=8)
+    ref = oracle_lib.compute_stats(d, st, a, threads=8)
+    for f in ("t0", "t1", "tc", "ig"):
+        assert np.array_equal(getattr(stats, f), ref[f]), f
+    assert diag["discarded"] == int(a["discarded"].sum())
+    assert diag["ic_filtered"] == int(a["ic_filtered"].sum())
