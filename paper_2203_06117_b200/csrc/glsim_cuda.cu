@@ -343,6 +343,7 @@ struct gs_engine {
   unsigned *cnt = nullptr;
   unsigned long long *tbase = nullptr;
   unsigned *init = nullptr;
+  unsigned *wlen32 = nullptr;
   void *data = nullptr;
   int64_t data_bytes = 0;
   int64_t pool_bytes = 0;            // requested gate-pool bytes
@@ -363,7 +364,7 @@ struct gs_engine {
   int64_t chunk_hint = 0;
   gs_timing last{};
 
-  void release_meta() { dfree(cnt); dfree(tbase); dfree(init); meta_windows = 0; }
+  void release_meta() { dfree(cnt); dfree(tbase); dfree(init); dfree(wlen32); meta_windows = 0; }
   void release_arena() {
     dfree(a_cnt); dfree(a_peak); dfree(a_filt); dfree(a_icf); dfree(a_disc); dfree(a_off);
     dfree(a_init); arena_windows = 0;
@@ -454,6 +455,7 @@ int ensure_meta(gs_engine *e, int64_t wins) {
   TRY(dalloc(&e->cnt, (size_t)(N * Wpad)));
   TRY(dalloc(&e->tbase, (size_t)(N * (Wpad / kTile))));
   TRY(dalloc(&e->init, (size_t)(N * (Wpad / 32))));
+  TRY(dalloc(&e->wlen32, (size_t)Wpad));
   e->meta_windows = Wpad;
   return GS_OK;
 }
@@ -580,6 +582,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     C.cnt = e->cnt;
     C.tbase = e->tbase;
     C.init = e->init;
+    C.wlen32 = e->wlen32;
     C.data = e->data;
     C.pool_base = (unsigned long long)(pi_bytes / (int64_t)sizeof(TS));
     C.block_words = (unsigned long long)block_words;
@@ -609,6 +612,10 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     CK(cudaMemsetAsync(e->work, 0, sizeof(unsigned) * (D->L * 5 + 1), e->st));
     CK(cudaMemsetAsync(e->err, 0, sizeof(int) * ERR_NFLAGS, e->st));
     CK(cudaEventRecord(e->ev[0], e->st));
+    if (narrow) {
+      chunk_windows<<<(int)((Wpad + 255) / 256), 256, 0, e->st>>>(C);
+      CK(cudaGetLastError());
+    }
     // ---- K1
     int k1 = 0;
     if (s->P > 0) {

@@ -92,6 +92,7 @@ struct ChunkDev {
   int N, Wc, Tc, Wpad;         // nets, windows, 128-tiles, cnt row pitch (= Tc*128)
   long long w0;                // absolute index of the chunk's first window
   const long long *bnd;        // [W+1] absolute window boundaries
+  unsigned *wlen32;            // [Wpad] chunk window lengths (narrow runs; 0 past Wc)
   unsigned *cnt;
   unsigned long long *tbase;
   unsigned *init;
@@ -757,11 +758,17 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
     ux += ub[j];
   }
   if (lane == kWarp - 1) S.ubo[kTile] = UB;
+  unsigned wl32[kWPL];
+  if constexpr (sizeof(TT) == 4) load_counts(C.wlen32 + base_w + wl, wl32);
 #pragma unroll
   for (int j = 0; j < kWPL; ++j) {
     S.idx0[wl + j] = (unsigned short)ix[j];
     const int wr = base_w + wl + j;
-    S.wlen[wl + j] = wr < C.Wc ? (TT)(C.bnd[C.w0 + wr + 1] - C.bnd[C.w0 + wr]) : (TT)0;
+    if constexpr (sizeof(TT) == 4) {
+      S.wlen[wl + j] = (TT)wl32[j];
+    } else {
+      S.wlen[wl + j] = wr < C.Wc ? (TT)(C.bnd[C.w0 + wr + 1] - C.bnd[C.w0 + wr]) : (TT)0;
+    }
   }
   if (lane == 0) S.next = 0;
   // Staging: fanin segments (UB words) then outputs (UB words) in the smem
@@ -1044,6 +1051,12 @@ gate_eval(DesignDev D, ChunkDev C, LevelArgs A) {
 template <typename TS, typename TT, int K>
 constexpr size_t eval_smem_bytes() {
   return sizeof(TileSmem<TS, TT, (K > 0 ? K : kMaxK)>) * kEvalWarps;
+}
+
+// per-chunk 32-bit window lengths (narrow runs), zero past the chunk end
+__global__ void chunk_windows(ChunkDev C) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < C.Wpad; w += gridDim.x * blockDim.x)
+    C.wlen32[w] = w < C.Wc ? (unsigned)(C.bnd[C.w0 + w + 1] - C.bnd[C.w0 + w]) : 0u;
 }
 
 // chunk accumulators -> run accumulators [t1 | tc | ig | filtered, icf, disc]
