@@ -507,6 +507,24 @@ __device__ __forceinline__ void record_arena(const ChunkDev &C, int g, int wr, i
   }
 }
 
+// output delay for the switching pin set sw and post-transition inputs idx
+template <typename TS, typename TT, int K>
+__device__ __forceinline__ TT event_delay(const DesignDev &D,
+                                          const TileSmem<TS, TT, (K > 0 ? K : kMaxK)> &S,
+                                          const int *arc, int kk, unsigned sw, unsigned idx,
+                                          int col) {
+  if constexpr (K > 0 && K <= 4 && sizeof(TT) == 4) {
+    return (TT)S.dtab[(((sw << K) | idx) << 1) | (unsigned)col];
+  } else {
+    TT dly = 0;
+    constexpr int KM = K > 0 ? K : kMaxK;
+#pragma unroll
+    for (int p = 0; p < KM; ++p)
+      if (p < kk && ((sw >> p) & 1u)) dly = max(dly, pin_delay<TS, TT, K>(D, S, arc, p, idx, col));
+    return dly;
+  }
+}
+
 template <typename TS, typename TT, int MODE, int K, bool PCT100, bool SMEM>
 __device__ __forceinline__ void event_loop(
     const DesignDev &D, const ChunkDev &C, int g, int kk, unsigned long long lut, const TT *ic,
@@ -845,47 +863,76 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
     pt1 = clock64();
     GS_PROF_ADD(PF_PHASE1, pt1 - pt0);
 #endif
-    // Windows left with at most one input transition need no event loop: with
-    // no earlier output edge there is nothing to retract, so the window
-    // holds exactly one output edge (t + ic + arc delay) if the function
-    // changes and the edge lands inside the window, else none.  The others go
-    // to the work list of the event loop.
+    // Windows left with at most two surviving input transitions need no event
+    // loop.  With no edge pending at the first event, Algo. 1's output side
+    // (K:136-203) collapses to a few selects: event 1 (both pins when the two
+    // transitions coincide) can only emit; event 2 can emit, cancel event 1's
+    // edge, or leave it pending; no stored edge can be popped.  Branch-free,
+    // so every lane runs the same short sequence whatever its window holds.
     unsigned trivial = 0;
-#pragma unroll
+#pragma unroll 1
     for (int j = 0; j < kWPL; ++j) {
       const int w = wl + j;
-      if (w >= nact) continue;
-      unsigned nt = 0, pin = 0, at = 0;
+      unsigned nt = 0, pa = 0, pb = 0, ia = 0, ib = 0;
 #pragma unroll
       for (int p = 0; p < kk; ++p) {
-        const unsigned a = S.offs[p][w], e = S.fend[p][w];
-        if (e > a) { pin = (unsigned)p; at = inb_off[p] + a; }
-        nt += e - a;
+        const unsigned a = S.offs[p][w], n = S.fend[p][w] - a;
+        // first / second transition of the window, in pin order
+        pa = (n >= 1 && nt == 0) ? (unsigned)p : pa;
+        ia = (n >= 1 && nt == 0) ? inb_off[p] + a : ia;
+        pb = ((n >= 1 && nt == 1) || (n >= 2 && nt == 0)) ? (unsigned)p : pb;
+        ib = (n >= 1 && nt == 1) ? inb_off[p] + a : (n >= 2 && nt == 0) ? inb_off[p] + a + 1 : ib;
+        nt += n;
       }
-      if (nt > 1) continue;
+      if (w >= nact || nt > 2) continue;
       trivial |= 1u << j;
-      const unsigned idx = S.idx0[w];
-      const unsigned y0 = lut_bit(lut, kk, D.lut_words, idx);
-      int cnt = 0, disc = 0;
+      // staged u32 values are arrival times already; u64 ones get ic added
+      TT ta = (TT)S.slab[ia] + (sizeof(TT) == 4 ? (TT)0 : ic[pa]);
+      TT tb = (TT)S.slab[ib] + (sizeof(TT) == 4 ? (TT)0 : ic[pb]);
+      const bool sw2 = nt == 2 && tb < ta;
+      { const TT tt = sw2 ? tb : ta; tb = sw2 ? ta : tb; ta = tt; }
+      { const unsigned pp = sw2 ? pb : pa; pb = sw2 ? pa : pb; pa = pp; }
+      // two transitions of one pin at one instant stay two events
+      const bool both = nt == 2 && ta == tb && pa != pb;
+      const bool n1 = nt >= 1, n2 = nt == 2 && !both;
+      const unsigned s1 = (1u << pa) | (both ? (1u << pb) : 0u), s2 = 1u << pb;
+      const unsigned i0 = S.idx0[w];
+      const unsigned i1 = i0 ^ (n1 ? s1 : 0u), i2 = i1 ^ (n2 ? s2 : 0u);
+      const unsigned y0 = lut_bit(lut, kk, D.lut_words, i0);
+      const unsigned y1 = lut_bit(lut, kk, D.lut_words, i1);
+      const unsigned y2 = lut_bit(lut, kk, D.lut_words, i2);
+      const bool c1 = y1 != y0, c2 = y2 != y1;
+      const TT d2 = event_delay<TS, TT, K>(D, S, arc, kk, s2, i2, y2 ? 0 : 1);
+      const TT o1 = ta + event_delay<TS, TT, K>(D, S, arc, kk, s1, i1, y1 ? 0 : 1);
+      const TT o2 = tb + d2;
+      const TT thr = PCT100 ? d2 : (TT)((unsigned long long)d2 * (unsigned)pct / 100u);
+      const TT wlen = S.wlen[w];
+      const bool x2 = c2 && c1 && (o2 <= o1 || o2 - o1 < thr);   // edge 1 cancelled
+      const bool e2 = c2 && !x2;                                 // edge 2 emitted
+      const bool in1 = o1 < wlen, in2 = o2 < wlen;
+      const bool st1 = e2 && c1 && in1;                          // edge 1 stored at event 2
+      const TT tp = e2 ? o2 : o1;                                // pending at the end
+      const bool fl = e2 ? in2 : (c1 && !x2 && in1);             // ... and flushed
+      const unsigned cnt = (st1 ? 1u : 0u) + (fl ? 1u : 0u);
+      const TT f0 = st1 ? o1 : tp;
       TS *st = S.slab + UB + S.ubo[w];
-      if (nt == 1) {
-        const unsigned idx1 = idx ^ (1u << pin);
-        const unsigned y1 = lut_bit(lut, kk, D.lut_words, idx1);
-        if (y1 != y0) {
-          const TT t_out = (TT)S.slab[at] + (sizeof(TT) == 4 ? (TT)0 : ic[pin]) +
-                           pin_delay<TS, TT, K>(D, S, arc, (int)pin, idx1, y1 ? 0 : 1);
-          if (t_out < S.wlen[w]) { st[0] = (TS)t_out; cnt = 1; } else { disc = 1; }
-          if (PCT100 && cnt) acc_t1 += y0 ? (long long)t_out : (long long)(S.wlen[w] - t_out);
-        }
+      if (cnt >= 1) st[0] = (TS)f0;
+      if (cnt == 2) st[1] = (TS)tp;
+      const int disc = (c1 && !in1 ? 1 : 0) + (e2 && !in2 ? 1 : 0) - (x2 && !in1 ? 1 : 0);
+      if (PCT100) {
+        const TT on = cnt == 0 ? (y0 ? wlen : (TT)0)
+                    : cnt == 1 ? (y0 ? f0 : wlen - f0)
+                               : (y0 ? f0 + (wlen - tp) : tp - f0);
+        acc_t1 += (long long)on;
       }
-      if (PCT100 && !cnt && y0) acc_t1 += (long long)S.wlen[w];
-      S.cnt[w] = (unsigned)cnt;
+      S.cnt[w] = cnt;
       S.y0[w] = (unsigned char)y0;
       acc_tc += cnt;
+      acc_filt += x2 ? 1 : 0;
       acc_disc += disc;
       acc_icf += S.icfw[w];
-      record_arena<MODE, TS>(C, g, base_w + w, cnt, cnt, 0, (int)S.icfw[w], disc, y0,
-                             [&](int q) { return st[q]; });
+      record_arena<MODE, TS>(C, g, base_w + w, (int)cnt, (int)cnt, x2 ? 1 : 0, (int)S.icfw[w],
+                             disc, y0, [&](int q) -> TS & { return st[q]; });
     }
     // compact the remaining windows into the work list
     unsigned m = 0;
