@@ -816,7 +816,8 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
       // pair filter below only compares differences, so it is unaffected
 #pragma unroll
       for (int p = 0; p < kk; ++p)
-        for (unsigned i = lane; i < tot[p]; i += kWarp) S.slab[inb_off[p] + i] += (TS)ic[p];
+        if (ic[p] != 0)
+          for (unsigned i = lane; i < tot[p]; i += kWarp) S.slab[inb_off[p] + i] += (TS)ic[p];
     }
     stage = S.slab + UB;
     __syncwarp();
@@ -831,6 +832,33 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
 #pragma unroll
     for (int p = 0; p < kk; ++p) {
       const TT d = ic[p];
+      // Cheap exact check first: a lane's kWPL windows are one contiguous run
+      // of the segment, so one pass over it (skipping the pairs that straddle
+      // a window boundary) finds whether any pair is narrower than d.  Most
+      // tiles have none -- gate outputs are already spaced by their own
+      // inertial delays -- and then the segment is left as staged.
+      bool narrow = false;
+      if (d > 0) {
+        unsigned bo[kWPL + 1];
+#pragma unroll
+        for (int j = 0; j <= kWPL; ++j) bo[j] = inb_off[p] + S.offs[p][wl + j];
+        if (bo[kWPL] > bo[0]) {
+          TT prev = (TT)S.slab[bo[0]];
+          for (unsigned i = bo[0] + 1; i < bo[kWPL]; ++i) {
+            const TT cur = (TT)S.slab[i];
+            bool edge = false;
+#pragma unroll
+            for (int j = 1; j < kWPL; ++j) edge |= i == bo[j];
+            narrow |= !edge && cur - prev < d;
+            prev = cur;
+          }
+        }
+      }
+      if (!__any_sync(0xffffffffu, narrow)) {
+#pragma unroll
+        for (int j = 0; j < kWPL; ++j) S.fend[p][wl + j] = (unsigned short)S.offs[p][wl + j + 1];
+        continue;
+      }
 #pragma unroll
       for (int j = 0; j < kWPL; ++j) {
         const unsigned a = inb_off[p] + S.offs[p][wl + j];
