@@ -610,10 +610,92 @@ __device__ __forceinline__ void event_loop(
     TT tmin = nxt[0];
 #pragma unroll
     for (int p = 1; p < kk; ++p) tmin = min(tmin, nxt[p]);
-    if (tmin == INF) {
-      // window exhausted: flush the pending edge, record the window
+    if (SMEM || tmin != INF) {  // staged loop windows hold >= 3 transitions
+      // multiple simultaneous inputs: consume every pin arriving at tmin, then
+      // advance those pins to their next transition
+      unsigned sw = 0;
+#pragma unroll
+      for (int p = 0; p < kk; ++p) sw |= (nxt[p] == tmin ? 1u : 0u) << p;
+      idx ^= sw;
+#pragma unroll
+      for (int p = 0; p < kk; ++p) {
+        const bool hit = (sw >> p) & 1u;
+        if constexpr (SMEM) {
+          // branch-free: the staged segment is in bounds of the slab even when
+          // exhausted, so the load is unconditional and the result selected
+          cur[p] += hit ? 1u : 0u;
+          const TT v = in_at(p, cur[p]) + (sizeof(TT) == 4 ? (TT)0 : ic[p]);
+          nxt[p] = hit ? (cur[p] < end[p] ? v : INF) : nxt[p];
+        } else if (hit) {
+          cur[p] += 1;
+          refresh(p);
+        }
+      }
+      // Output side (K:136-193), as selects rather than branches so the lanes
+      // of the warp stay converged: schedule the edge through the inertial
+      // filter; cancel the pulse, or keep the previous edge and make this one
+      // the pending edge (discarded when it lands at or past the window end).
+      const unsigned ny = lut_bit(lut, kk, D.lut_words, idx);
+      const bool chg = ny != y;
+      const int col = ny ? 0 : 1;
+      TT dly = 0;
+      if constexpr (K > 0 && K <= 4 && sizeof(TT) == 4) {
+        dly = (TT)S.dtab[(((sw << K) | idx) << 1) | (unsigned)col];
+      } else {
+#pragma unroll
+        for (int p = 0; p < kk; ++p)
+          if ((sw >> p) & 1u) dly = max(dly, pin_delay<TS, TT, K>(D, S, arc, p, idx, col));
+      }
+      const TT t_out = tmin + dly;
+      const TT thr = PCT100 ? dly : (TT)((unsigned long long)dly * (unsigned)pct / 100u);
+      bool cancel;
+      if constexpr (PCT100) {
+        // event times strictly increase, so with no pending edge the newest
+        // stored edge (stored when a later edge survived against it) is never
+        // closer than the new edge's own delay: only the pending edge can be
+        // cancelled, and stored edges are final
+        cancel = chg && has_last && (t_out <= t_last || t_out - t_last < thr);
+      } else {
+        const bool have = has_last || cnt > 0;
+        const TT tgt = has_last ? t_last : t_stored;
+        cancel = chg && have && (t_out <= tgt || t_out - tgt < thr);
+      }
+      const bool emit = chg && !cancel;
+      // cancellation: drop the pending edge, or (below 100 %) pop a stored one
+      // whose predecessor becomes the retraction target
+      const bool pop = !PCT100 && cancel && !has_last;
+      disc -= (cancel && has_last && !last_stored) ? 1 : 0;
+      if (!PCT100) {
+        cnt -= pop ? 1 : 0;
+        if (pop && cnt > 0) t_stored = (TT)out_at(cnt - 1);
+      }
+      filt += cancel ? 1 : 0;
+      // emission: the previous pending edge (if it landed in the window) is stored
+      const bool store = emit && has_last && last_stored;
+      if (store && cnt < cap) out_at(cnt) = (TS)t_last;
+      ovf |= store && cnt >= cap;
+      if (!PCT100) t_stored = store ? t_last : t_stored;
+      cnt += store ? 1 : 0;
+      if (MODE != MODE_STATS) peak = max(peak, cnt);
+      t1w += (store && dv) ? t_last - dt : (TT)0;
+      dv ^= store ? 1u : 0u;
+      dt = store ? t_last : dt;
+      const bool inwin = t_out < wlen;
+      disc += (emit && !inwin) ? 1 : 0;
+      last_stored = emit ? inwin : last_stored;
+      t_last = emit ? t_out : t_last;
+      has_last = emit || (has_last && !cancel);
+      y = chg ? ny : y;
+    }
+    // window exhausted (checked right after its last event, so finishing a
+    // window does not cost a loop iteration of its own): flush the pending
+    // edge, record the window
+    TT tn = nxt[0];
+#pragma unroll
+    for (int p = 1; p < kk; ++p) tn = min(tn, nxt[p]);
+    if (tn == INF) {
       if (has_last && last_stored) {
-        if (cnt < cap) out_at(cnt) = (TS)t_last; else atomicExch(C.err + ERR_CAP, 1);
+        if (cnt < cap) out_at(cnt) = (TS)t_last; else ovf = true;
         ++cnt;
         peak = max(peak, cnt);
         t1w += dv ? t_last - dt : (TT)0;
@@ -630,83 +712,7 @@ __device__ __forceinline__ void event_loop(
       record_arena<MODE, TS>(C, g, base_w + w, cnt, peak, filt, icf, disc, y0,
                              [&](int j) { return out_at(j); });
       has = false;
-      continue;
     }
-    // multiple simultaneous inputs: consume every pin arriving at tmin, then
-    // advance those pins to their next transition
-    unsigned sw = 0;
-#pragma unroll
-    for (int p = 0; p < kk; ++p) sw |= (nxt[p] == tmin ? 1u : 0u) << p;
-    idx ^= sw;
-#pragma unroll
-    for (int p = 0; p < kk; ++p) {
-      const bool hit = (sw >> p) & 1u;
-      if constexpr (SMEM) {
-        // branch-free: the staged segment is in bounds of the slab even when
-        // exhausted, so the load is unconditional and the result selected
-        cur[p] += hit ? 1u : 0u;
-        const TT v = in_at(p, cur[p]) + (sizeof(TT) == 4 ? (TT)0 : ic[p]);
-        nxt[p] = hit ? (cur[p] < end[p] ? v : INF) : nxt[p];
-      } else if (hit) {
-        cur[p] += 1;
-        refresh(p);
-      }
-    }
-    // Output side (K:136-193), as selects rather than branches so the lanes
-    // of the warp stay converged: schedule the edge through the inertial
-    // filter; cancel the pulse, or keep the previous edge and make this one
-    // the pending edge (discarded when it lands at or past the window end).
-    const unsigned ny = lut_bit(lut, kk, D.lut_words, idx);
-    const bool chg = ny != y;
-    const int col = ny ? 0 : 1;
-    TT dly = 0;
-    if constexpr (K > 0 && K <= 4 && sizeof(TT) == 4) {
-      dly = (TT)S.dtab[(((sw << K) | idx) << 1) | (unsigned)col];
-    } else {
-#pragma unroll
-      for (int p = 0; p < kk; ++p)
-        if ((sw >> p) & 1u) dly = max(dly, pin_delay<TS, TT, K>(D, S, arc, p, idx, col));
-    }
-    const TT t_out = tmin + dly;
-    const TT thr = PCT100 ? dly : (TT)((unsigned long long)dly * (unsigned)pct / 100u);
-    bool cancel;
-    if constexpr (PCT100) {
-      // event times strictly increase, so with no pending edge the newest
-      // stored edge (stored when a later edge survived against it) is never
-      // closer than the new edge's own delay: only the pending edge can be
-      // cancelled, and stored edges are final
-      cancel = chg && has_last && (t_out <= t_last || t_out - t_last < thr);
-    } else {
-      const bool have = has_last || cnt > 0;
-      const TT tgt = has_last ? t_last : t_stored;
-      cancel = chg && have && (t_out <= tgt || t_out - tgt < thr);
-    }
-    const bool emit = chg && !cancel;
-    // cancellation: drop the pending edge, or (below 100 %) pop a stored one
-    // whose predecessor becomes the retraction target
-    const bool pop = !PCT100 && cancel && !has_last;
-    disc -= (cancel && has_last && !last_stored) ? 1 : 0;
-    if (!PCT100) {
-      cnt -= pop ? 1 : 0;
-      if (pop && cnt > 0) t_stored = (TT)out_at(cnt - 1);
-    }
-    filt += cancel ? 1 : 0;
-    // emission: the previous pending edge (if it landed in the window) is stored
-    const bool store = emit && has_last && last_stored;
-    if (store && cnt < cap) out_at(cnt) = (TS)t_last;
-    ovf |= store && cnt >= cap;
-    if (!PCT100) t_stored = store ? t_last : t_stored;
-    cnt += store ? 1 : 0;
-    if (MODE != MODE_STATS) peak = max(peak, cnt);
-    t1w += (store && dv) ? t_last - dt : (TT)0;
-    dv ^= store ? 1u : 0u;
-    dt = store ? t_last : dt;
-    const bool inwin = t_out < wlen;
-    disc += (emit && !inwin) ? 1 : 0;
-    last_stored = emit ? inwin : last_stored;
-    t_last = emit ? t_out : t_last;
-    has_last = emit || (has_last && !cancel);
-    y = chg ? ny : y;
   }
   if (ovf) atomicExch(C.err + ERR_CAP, 1);
   acc_t1 += l_t1;
