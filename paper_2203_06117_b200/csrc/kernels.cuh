@@ -437,6 +437,31 @@ __device__ __forceinline__ long long arc_delay<long long>(const DesignDev &D, in
 }
 
 // per-warp shared-memory tile state
+// one lane's kWPL = 4 consecutive per-window values <-> shared memory, as a
+// single vector access (the row and the lane's offset are 4-element aligned)
+static_assert(kWPL == 4, "st4/ld4 move 4 windows");
+__device__ __forceinline__ void st4(unsigned *p, const unsigned (&v)[4]) {
+  *reinterpret_cast<uint4 *>(p) = make_uint4(v[0], v[1], v[2], v[3]);
+}
+template <typename T, typename = typename std::enable_if<sizeof(T) == 8>::type>
+__device__ __forceinline__ void st4(T *p, const T (&v)[4]) {
+  reinterpret_cast<ulonglong2 *>(p)[0] =
+      make_ulonglong2((unsigned long long)v[0], (unsigned long long)v[1]);
+  reinterpret_cast<ulonglong2 *>(p)[1] =
+      make_ulonglong2((unsigned long long)v[2], (unsigned long long)v[3]);
+}
+__device__ __forceinline__ void st4(unsigned short *p, const unsigned (&v)[4]) {
+  *reinterpret_cast<uint2 *>(p) = make_uint2((v[0] & 0xFFFFu) | (v[1] << 16),
+                                             (v[2] & 0xFFFFu) | (v[3] << 16));
+}
+__device__ __forceinline__ void ld4(const unsigned *p, unsigned (&v)[4]) {
+  const uint4 x = *reinterpret_cast<const uint4 *>(p);
+  v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+}
+__device__ __forceinline__ unsigned ld4_u8(const unsigned char *p) {  // 4 bytes, packed
+  return *reinterpret_cast<const unsigned *>(p);
+}
+
 template <typename TS, typename TT, int KM>
 struct alignas(16) TileSmem {
   TS slab[kSlab];                  // staged fanin segments, then output staging
@@ -447,17 +472,19 @@ struct alignas(16) TileSmem {
   // once per gate so the event step does one lookup
   unsigned dtab[KM <= 4 ? (1 << (2 * KM)) * 2 : 1];
 
-  unsigned offs[KM][kTile + 1];    // per pin: window w's toggles start at offs[p][w]
-  unsigned short fend[KM][kTile];  // per pin: end of window w's toggles after the
-                                   // interconnect filter (smem-staged tiles)
-  unsigned short icfw[kTile];      // interconnect-filtered pairs per window
-  unsigned char work[kTile];       // windows left for the event loop
-  unsigned ubo[kTile + 1];         // output staging offsets: prefix of the per-window bound
-  TT wlen[kTile];                  // window lengths
-  unsigned cnt[kTile];             // stored toggles per window
-  unsigned short idx0[kTile];      // window-start input vector
-  unsigned char y0[kTile];         // window-start output value
-  unsigned next;                   // dynamic window counter
+  // per-window arrays: rows 16-byte aligned so a lane's kWPL = 4 windows
+  // move with one vector access (ld4 / st4)
+  alignas(16) unsigned offs[KM][kTile + 4];  // per pin: window w's toggles start at offs[p][w]
+  alignas(16) unsigned ubo[kTile + 4];       // output staging offsets: prefix of the bound
+  alignas(16) TT wlen[kTile];                // window lengths
+  alignas(16) unsigned cnt[kTile];           // stored toggles per window
+  alignas(16) unsigned short fend[KM][kTile];  // per pin: end of window w's toggles after
+                                               // the interconnect filter (staged tiles)
+  alignas(16) unsigned short icfw[kTile];    // interconnect-filtered pairs per window
+  alignas(16) unsigned short idx0[kTile];    // window-start input vector
+  alignas(16) unsigned char y0[kTile];       // window-start output value
+  unsigned char work[kTile];                 // windows left for the event loop
+  unsigned next;                             // dynamic window counter
 };
 
 // Phase 2 of K4: one lockstep loop over the tile's windows.  Every lane with
@@ -530,11 +557,11 @@ __device__ __forceinline__ void event_loop(
     const DesignDev &D, const ChunkDev &C, int g, int kk, unsigned long long lut, const TT *ic,
     const int *arc, int pct, TileSmem<TS, TT, (K > 0 ? K : kMaxK)> &S,
     const typename std::conditional<SMEM, unsigned, const TS *>::type *inb, TS *stage,
-    unsigned stage_off, bool ok, int base_w, int nwork, long long &acc_t1, long long &acc_tc,
+    unsigned stage_off, bool ok, int base_w, int nwork, long long &acc_t1,
     long long &acc_filt, long long &acc_icf, long long &acc_disc) {
   constexpr int KM = K > 0 ? K : kMaxK;
   const TT INF = TimeTraits<TT>::inf();
-  unsigned l_tc = 0, l_filt = 0, l_icf = 0, l_disc = 0;
+  unsigned l_filt = 0, l_icf = 0, l_disc = 0;
   long long l_t1 = 0;
   // dwell at 1 (dwell_sweep), accumulated as edges are stored; valid at 100 %
   // where a stored edge is final (below that, phase 3 recomputes it)
@@ -579,7 +606,7 @@ __device__ __forceinline__ void event_loop(
         w = SMEM ? (int)S.work[nw] : (int)nw;
         has = true;
         cnt = peak = filt = disc = 0;
-        icf = SMEM ? (int)S.icfw[w] : 0;
+        icf = (SMEM && MODE != MODE_STATS) ? (int)S.icfw[w] : 0;  // for record_arena
 #pragma unroll
         for (int p = 0; p < kk; ++p) {
           cur[p] = S.offs[p][w];
@@ -705,9 +732,8 @@ __device__ __forceinline__ void event_loop(
       if (PCT100) l_t1 += (long long)(t1w + (dv ? wlen - dt : (TT)0));
       S.cnt[w] = (unsigned)cnt;
       S.y0[w] = (unsigned char)y0;
-      l_tc += cnt;
       l_filt += filt;
-      l_icf += icf;
+      if (!SMEM) l_icf += icf;  // staged tiles: counted by the phase-1 filter
       l_disc += disc;
       record_arena<MODE, TS>(C, g, base_w + w, cnt, peak, filt, icf, disc, y0,
                              [&](int j) { return out_at(j); });
@@ -716,7 +742,6 @@ __device__ __forceinline__ void event_loop(
   }
   if (ovf) atomicExch(C.err + ERR_CAP, 1);
   acc_t1 += l_t1;
-  acc_tc += l_tc;
   acc_filt += l_filt;
   acc_icf += l_icf;
   acc_disc += l_disc;
@@ -760,12 +785,14 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
 #pragma unroll
     for (int j = 0; j < kWPL; ++j) s4 += c[j];
     unsigned ex = warp_excl_scan(s4, &tot[p]);
+    unsigned o4[kWPL];
 #pragma unroll
     for (int j = 0; j < kWPL; ++j) {
-      S.offs[p][wl + j] = ex;
+      o4[j] = ex;
       ex += c[j];
       ub[j] += c[j];
     }
+    st4(&S.offs[p][wl], o4);
     if (lane == kWarp - 1) S.offs[p][kTile] = tot[p];
     tb[p] = __ldg(C.tbase + (size_t)nn * C.Tc + t);
     const unsigned bits = load_init_bits(C.init + (size_t)nn * Tw, t);
@@ -776,23 +803,29 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
 #pragma unroll
   for (int j = 0; j < kWPL; ++j) us += ub[j];
   unsigned ux = warp_excl_scan(us, &UB);
+  {
+    unsigned u4[kWPL];
 #pragma unroll
-  for (int j = 0; j < kWPL; ++j) {
-    S.ubo[wl + j] = ux;
-    ux += ub[j];
+    for (int j = 0; j < kWPL; ++j) {
+      u4[j] = ux;
+      ux += ub[j];
+    }
+    st4(&S.ubo[wl], u4);
   }
   if (lane == kWarp - 1) S.ubo[kTile] = UB;
-  unsigned wl32[kWPL];
-  if constexpr (sizeof(TT) == 4) load_counts(C.wlen32 + base_w + wl, wl32);
+  st4(&S.idx0[wl], ix);
+  if constexpr (sizeof(TT) == 4) {
+    unsigned wl32[kWPL];
+    load_counts(C.wlen32 + base_w + wl, wl32);
+    st4(&S.wlen[wl], wl32);
+  } else {
+    TT w4[kWPL];
 #pragma unroll
-  for (int j = 0; j < kWPL; ++j) {
-    S.idx0[wl + j] = (unsigned short)ix[j];
-    const int wr = base_w + wl + j;
-    if constexpr (sizeof(TT) == 4) {
-      S.wlen[wl + j] = (TT)wl32[j];
-    } else {
-      S.wlen[wl + j] = wr < C.Wc ? (TT)(C.bnd[C.w0 + wr + 1] - C.bnd[C.w0 + wr]) : (TT)0;
+    for (int j = 0; j < kWPL; ++j) {
+      const int wr = base_w + wl + j;
+      w4[j] = wr < C.Wc ? (TT)(C.bnd[C.w0 + wr + 1] - C.bnd[C.w0 + wr]) : (TT)0;
     }
+    st4(&S.wlen[wl], w4);
   }
   if (lane == 0) S.next = 0;
   // Staging: fanin segments (UB words) then outputs (UB words) in the smem
@@ -861,8 +894,10 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
         }
       }
       if (!__any_sync(0xffffffffu, narrow)) {
+        unsigned e4[kWPL];
 #pragma unroll
-        for (int j = 0; j < kWPL; ++j) S.fend[p][wl + j] = (unsigned short)S.offs[p][wl + j + 1];
+        for (int j = 0; j < kWPL; ++j) e4[j] = S.offs[p][wl + j + 1];
+        st4(&S.fend[p][wl], e4);
         continue;
       }
 #pragma unroll
@@ -890,8 +925,9 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
         S.fend[p][wl + j] = (unsigned short)(e - inb_off[p]);
       }
     }
+    st4(&S.icfw[wl], f);
 #pragma unroll
-    for (int j = 0; j < kWPL; ++j) S.icfw[wl + j] = (unsigned short)f[j];
+    for (int j = 0; j < kWPL; ++j) acc_icf += f[j];
     __syncwarp();
 #ifdef GS_PROF
     pt1 = clock64();
@@ -903,7 +939,8 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
     // transitions coincide) can only emit; event 2 can emit, cancel event 1's
     // edge, or leave it pending; no stored edge can be popped.  Branch-free,
     // so every lane runs the same short sequence whatever its window holds.
-    unsigned trivial = 0;
+    unsigned trivial = 0, cf_filt = 0;
+    int cf_disc = 0;
 #pragma unroll 1
     for (int j = 0; j < kWPL; ++j) {
       const int w = wl + j;
@@ -954,20 +991,23 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
       if (cnt == 2) st[1] = (TS)tp;
       const int disc = (c1 && !in1 ? 1 : 0) + (e2 && !in2 ? 1 : 0) - (x2 && !in1 ? 1 : 0);
       if (PCT100) {
-        const TT on = cnt == 0 ? (y0 ? wlen : (TT)0)
-                    : cnt == 1 ? (y0 ? f0 : wlen - f0)
-                               : (y0 ? f0 + (wlen - tp) : tp - f0);
-        acc_t1 += (long long)on;
+        // dwell at 1: +-edge times by the value before each edge, plus the
+        // window end when the final value is 1 (wrapping arithmetic, exact
+        // since the result lies in [0, wlen])
+        const TT e0 = cnt >= 1 ? f0 : (TT)0, e1 = cnt == 2 ? tp : (TT)0;
+        const TT wf = (cnt & 1u) ? (y0 ? (TT)0 : wlen) : (y0 ? wlen : (TT)0);
+        acc_t1 += (long long)(y0 ? e0 - e1 + wf : e1 - e0 + wf);
       }
       S.cnt[w] = cnt;
       S.y0[w] = (unsigned char)y0;
-      acc_tc += cnt;
-      acc_filt += x2 ? 1 : 0;
-      acc_disc += disc;
-      acc_icf += S.icfw[w];
-      record_arena<MODE, TS>(C, g, base_w + w, (int)cnt, (int)cnt, x2 ? 1 : 0, (int)S.icfw[w],
-                             disc, y0, [&](int q) -> TS & { return st[q]; });
+      cf_filt += x2 ? 1u : 0u;
+      cf_disc += disc;
+      if (MODE != MODE_STATS)
+        record_arena<MODE, TS>(C, g, base_w + w, (int)cnt, (int)cnt, x2 ? 1 : 0,
+                               (int)S.icfw[w], disc, y0, [&](int q) -> TS & { return st[q]; });
     }
+    acc_filt += cf_filt;
+    acc_disc += cf_disc;
     // compact the remaining windows into the work list
     unsigned m = 0;
 #pragma unroll
@@ -1003,12 +1043,12 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   // ---- phase 2: one lockstep loop (see event_loop)
   if (in_smem) {
     event_loop<TS, TT, MODE, K, PCT100, true>(D, C, g, kk, lut, ic, arc, pct, S, inb_off, stage,
-                                              UB, ok, base_w, (int)nwork, acc_t1, acc_tc,
-                                              acc_filt, acc_icf, acc_disc);
+                                              UB, ok, base_w, (int)nwork, acc_t1, acc_filt,
+                                              acc_icf, acc_disc);
   } else {
     event_loop<TS, TT, MODE, K, PCT100, false>(D, C, g, kk, lut, ic, arc, pct, S, inb_glob,
                                                stage, 0, ok, base_w, (int)nwork, acc_t1,
-                                               acc_tc, acc_filt, acc_icf, acc_disc);
+                                               acc_filt, acc_icf, acc_disc);
   }
   __syncwarp();
 
@@ -1016,12 +1056,14 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   GS_PROF_ADD(PF_LOOP, pt3 - pt2);
   // ---- phase 3: compaction (warp scan of the lane's 4 windows' counts);
   // the copy out of the staging area also yields the dwell at 1 (dwell_sweep)
-  unsigned c[kWPL], nib = 0, s = 0;
+  unsigned c[kWPL], c4[kWPL], nib = 0, s = 0;
+  ld4(&S.cnt[wl], c4);
+  const unsigned y4 = ld4_u8(&S.y0[wl]);
 #pragma unroll
   for (int j = 0; j < kWPL; ++j) {
     const bool act = wl + j < nact;
-    c[j] = act ? S.cnt[wl + j] : 0u;
-    nib |= (act ? (unsigned)S.y0[wl + j] : 0u) << j;
+    c[j] = act ? c4[j] : 0u;
+    nib |= (act ? (y4 >> (8 * j)) & 1u : 0u) << j;
     s += c[j];
   }
   unsigned CNT;
@@ -1057,6 +1099,7 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
     dst += c[j];
   }
   acc_t1 += t1;
+  acc_tc += s;
   __syncwarp();
   GS_PROF_T(pt4);
   GS_PROF_ADD(PF_PHASE3, pt4 - pt3);
