@@ -571,8 +571,8 @@ __device__ __forceinline__ void event_loop(
   bool has = false, more = ok;
   unsigned cur[KM] = {}, end[KM] = {}, idx = 0, y = 0, y0 = 0, so = 0;
   TT nxt[KM] = {}, wlen = 0, t_last = 0, t_stored = 0;
-  int cnt = 0, peak = 0, filt = 0, icf = 0, disc = 0, cap = 0;
-  bool has_last = false, last_stored = false, ovf = false;
+  int cnt = 0, peak = 0, filt = 0, icf = 0, disc = 0;
+  bool has_last = false, last_stored = false;
   auto in_at = [&](int p, unsigned q) -> TT {
     if constexpr (SMEM) return (TT)S.slab[inb[p] + q];
     else return (TT)__ldg(inb[p] + q);
@@ -617,7 +617,6 @@ __device__ __forceinline__ void event_loop(
         y0 = y = lut_bit(lut, kk, D.lut_words, idx);
         wlen = S.wlen[w];
         so = S.ubo[w];
-        cap = (int)(S.ubo[w + 1] - so);  // peak <= #events <= fanin toggles
         has_last = last_stored = false;
         dv = y0;
         dt = t1w = 0;
@@ -699,8 +698,10 @@ __device__ __forceinline__ void event_loop(
       filt += cancel ? 1 : 0;
       // emission: the previous pending edge (if it landed in the window) is stored
       const bool store = emit && has_last && last_stored;
-      if (store && cnt < cap) out_at(cnt) = (TS)t_last;
-      ovf |= store && cnt >= cap;
+      // (in bounds: a stored edge is one emission, an emission one event, and
+      // the window's staging bound ubo[w+1] - ubo[w] counts every fanin
+      // toggle, so cnt never reaches it)
+      if (store) out_at(cnt) = (TS)t_last;
       if (!PCT100) t_stored = store ? t_last : t_stored;
       cnt += store ? 1 : 0;
       if (MODE != MODE_STATS) peak = max(peak, cnt);
@@ -722,7 +723,7 @@ __device__ __forceinline__ void event_loop(
     for (int p = 1; p < kk; ++p) tn = min(tn, nxt[p]);
     if (tn == INF) {
       if (has_last && last_stored) {
-        if (cnt < cap) out_at(cnt) = (TS)t_last; else ovf = true;
+        out_at(cnt) = (TS)t_last;
         ++cnt;
         peak = max(peak, cnt);
         t1w += dv ? t_last - dt : (TT)0;
@@ -740,7 +741,6 @@ __device__ __forceinline__ void event_loop(
       has = false;
     }
   }
-  if (ovf) atomicExch(C.err + ERR_CAP, 1);
   acc_t1 += l_t1;
   acc_filt += l_filt;
   acc_icf += l_icf;
@@ -1081,9 +1081,20 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
     if (wl + j >= nact) continue;
     const TS *src = stage + S.ubo[wl + j];
     if (PCT100) {
-      // dwell already accumulated in phases 1 and 2
-      if (wrote)
-        for (unsigned q = 0; q < c[j]; ++q) dst[q] = src[q];
+      // dwell already accumulated in phases 1 and 2.  Most windows store at
+      // most two edges: those go as two predicated stores (the staged reads
+      // stay inside the smem tile even past the window's bound), the rest
+      // continue in a loop
+      if (wrote) {
+        unsigned q = 0;
+        if (in_smem) {
+          const TS a0 = src[0], a1 = src[1];
+          if (c[j] > 0) dst[0] = a0;
+          if (c[j] > 1) dst[1] = a1;
+          q = 2;
+        }
+        for (; q < c[j]; ++q) dst[q] = src[q];
+      }
     } else {
       unsigned v = (nib >> j) & 1u;
       long long prev = 0;
