@@ -939,11 +939,34 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
     // transitions coincide) can only emit; event 2 can emit, cancel event 1's
     // edge, or leave it pending; no stored edge can be popped.  Branch-free,
     // so every lane runs the same short sequence whatever its window holds.
-    unsigned trivial = 0, cf_filt = 0;
+    // The windows are first split into two lists (loop windows at the front
+    // of `work`, closed-form ones behind them), so the closed form runs in
+    // ceil(n / 32) rounds of one window per lane rather than kWPL rounds.
+    {
+      unsigned ntr[kWPL];
+#pragma unroll
+      for (int j = 0; j < kWPL; ++j) ntr[j] = 0;
+#pragma unroll
+      for (int p = 0; p < kk; ++p)
+#pragma unroll
+        for (int j = 0; j < kWPL; ++j) ntr[j] += S.fend[p][wl + j] - S.offs[p][wl + j];
+      unsigned cl = 0;  // (loop windows) | (closed-form windows) << 16
+#pragma unroll
+      for (int j = 0; j < kWPL; ++j)
+        if (wl + j < nact) cl += ntr[j] > 2 ? 1u : 1u << 16;
+      unsigned tot2;
+      unsigned x = warp_excl_scan(cl, &tot2);
+      nwork = tot2 & 0xFFFFu;
+      unsigned xl = x & 0xFFFFu, xt = nwork + (x >> 16);
+#pragma unroll
+      for (int j = 0; j < kWPL; ++j)
+        if (wl + j < nact) S.work[ntr[j] > 2 ? xl++ : xt++] = (unsigned char)(wl + j);
+    }
+    __syncwarp();
+    unsigned cf_filt = 0;
     int cf_disc = 0;
-#pragma unroll 1
-    for (int j = 0; j < kWPL; ++j) {
-      const int w = wl + j;
+    for (unsigned i = nwork + lane; i < (unsigned)nact; i += kWarp) {
+      const int w = S.work[i];
       unsigned nt = 0, pa = 0, pb = 0, ia = 0, ib = 0;
 #pragma unroll
       for (int p = 0; p < kk; ++p) {
@@ -955,8 +978,6 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
         ib = (n >= 1 && nt == 1) ? inb_off[p] + a : (n >= 2 && nt == 0) ? inb_off[p] + a + 1 : ib;
         nt += n;
       }
-      if (w >= nact || nt > 2) continue;
-      trivial |= 1u << j;
       // staged u32 values are arrival times already; u64 ones get ic added
       TT ta = (TT)S.slab[ia] + (sizeof(TT) == 4 ? (TT)0 : ic[pa]);
       TT tb = (TT)S.slab[ib] + (sizeof(TT) == 4 ? (TT)0 : ic[pb]);
@@ -1008,14 +1029,6 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
     }
     acc_filt += cf_filt;
     acc_disc += cf_disc;
-    // compact the remaining windows into the work list
-    unsigned m = 0;
-#pragma unroll
-    for (int j = 0; j < kWPL; ++j) m += (wl + j < nact && !((trivial >> j) & 1u)) ? 1u : 0u;
-    unsigned mx = warp_excl_scan(m, &nwork);
-#pragma unroll
-    for (int j = 0; j < kWPL; ++j)
-      if (wl + j < nact && !((trivial >> j) & 1u)) S.work[mx++] = (unsigned char)(wl + j);
   } else {
 #pragma unroll
     for (int p = 0; p < kk; ++p) inb_glob[p] = data + tb[p];
