@@ -61,6 +61,22 @@ int upload(T **p, const T *src, size_t n) {
   return GS_OK;
 }
 
+// run a validation kernel that ORs flags into a device int; return the flags
+template <typename F>
+int device_check(int *flags, F launch) {
+  int *f = nullptr;
+  TRY(dalloc(&f, 1));
+  cudaError_t e = cudaMemset(f, 0, sizeof(int));
+  if (e == cudaSuccess) {
+    launch(f);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(flags, f, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(f);
+  if (e != cudaSuccess) return fail(GS_ERR_CUDA, cudaGetErrorString(e));
+  return GS_OK;
+}
+
 int use_device(int dev) {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
@@ -296,35 +312,33 @@ static int stim_build(gs_design *D, const gs_stim_desc *s, gs_stim *S) {
   if (S->csr) {
     if (!s->pi_times || !s->pi_init) return fail(GS_ERR_ARG, "incomplete CSR stimulus");
     if (s->pi_off[0] != 0) return fail(GS_ERR_ARG, "pi_off[0] must be 0");
-    for (int64_t p = 0; p < P; ++p) {
+    for (int64_t p = 0; p < P; ++p)
       if (s->pi_off[p + 1] < s->pi_off[p]) return fail(GS_ERR_ARG, "pi_off not monotone");
-      for (int64_t i = s->pi_off[p] + 1; i < s->pi_off[p + 1]; ++i)
-        if (s->pi_times[i] <= s->pi_times[i - 1])
-          return fail(GS_ERR_ARG, "input toggle times must be strictly increasing");
-    }
     S->n_toggles = s->pi_off[P];
     TRY(upload(&S->pi_off, (const long long *)s->pi_off, P + 1));
     TRY(upload(&S->pi_times, (const long long *)s->pi_times, S->n_toggles));
     TRY(upload(&S->pi_init, s->pi_init, P));
+    int bad = 0;
+    TRY(device_check(&bad, [&](int *flag) {
+      stim_check_csr<<<std::max<int64_t>(1, std::min<int64_t>((P + 7) / 8, 4096)), 256>>>(
+          S->pi_off, S->pi_times, (int)P, flag);
+    }));
+    if (bad) return fail(GS_ERR_ARG, "input toggle times must be strictly increasing");
   } else {
     if (!s->buf && s->n_buf) return fail(GS_ERR_ARG, "missing stimulus buffer");
     if (!s->offsets || !s->counts || !s->initials) return fail(GS_ERR_ARG, "incomplete windowed stimulus");
-    for (int64_t i = 0; i < P * W; ++i) {
-      if (s->counts[i] < 0 || s->offsets[i] < 0 || s->offsets[i] + s->counts[i] > s->n_buf)
-        return fail(GS_ERR_ARG, "stimulus window region out of range");
-      const int64_t w = i % W;
-      for (int64_t j = 0; j < s->counts[i]; ++j) {
-        const int64_t t = s->buf[s->offsets[i] + j];
-        if (t < S->bnd_host[w] || t >= S->bnd_host[w + 1] ||
-            (j && t <= s->buf[s->offsets[i] + j - 1]))
-          return fail(GS_ERR_ARG, "stimulus toggle outside its window or not increasing");
-      }
-    }
     S->n_toggles = s->n_buf;
     TRY(upload(&S->buf, (const long long *)s->buf, s->n_buf));
     TRY(upload(&S->offsets, (const long long *)s->offsets, P * W));
     TRY(upload(&S->counts, (const long long *)s->counts, P * W));
     TRY(upload(&S->initials, s->initials, P * W));
+    int bad = 0;
+    TRY(device_check(&bad, [&](int *flag) {
+      stim_check_win<<<(int)std::max<int64_t>(1, std::min<int64_t>((P * W + 255) / 256, 4096)),
+                       256>>>(S->buf, s->n_buf, S->offsets, S->counts, S->bnd, W, P * W, flag);
+    }));
+    if (bad & BAD_REGION) return fail(GS_ERR_ARG, "stimulus window region out of range");
+    if (bad) return fail(GS_ERR_ARG, "stimulus toggle outside its window or not increasing");
   }
   return GS_OK;
 }

@@ -275,6 +275,47 @@ __device__ __forceinline__ void store_counts(unsigned *p, const unsigned *c, boo
         keep ? make_uint4(c[4 * q], c[4 * q + 1], c[4 * q + 2], c[4 * q + 3]) : make_uint4(0, 0, 0, 0);
 }
 
+// ----------------------------------------------------------------- K0
+// Stimulus validation for gs_stim_create, on the device so a large stimulus
+// is not walked by one host thread: per input, toggle times strictly
+// increasing (CSR form; StimulusSet.build / Waveform invariants,
+// waveform.py:243-265); per (input, window), the region inside the buffer and
+// its toggles inside the window, increasing (windowed form, WF:49-63).
+enum StimBad { BAD_ORDER = 1, BAD_REGION = 2, BAD_WINDOW = 4 };
+
+__global__ void stim_check_csr(const long long *__restrict__ off,
+                               const long long *__restrict__ t, int P, int *bad) {
+  const int warps = gridDim.x * (blockDim.x / kWarp);
+  for (int p = blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp; p < P; p += warps) {
+    const long long hi = off[p + 1];
+    bool ok = true;
+    for (long long i = off[p] + 1 + lane_id(); i < hi; i += kWarp) ok &= t[i] > t[i - 1];
+    if (!__all_sync(0xffffffffu, ok) && lane_id() == 0) atomicOr(bad, BAD_ORDER);
+  }
+}
+
+__global__ void stim_check_win(const long long *__restrict__ buf, long long nbuf,
+                               const long long *__restrict__ offs,
+                               const long long *__restrict__ cnts,
+                               const long long *__restrict__ bnd, long long W, long long PW,
+                               int *bad) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < PW;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long o = offs[i], c = cnts[i], w = i % W;
+    if (c < 0 || o < 0 || o + c > nbuf) {
+      atomicOr(bad, BAD_REGION);
+      continue;
+    }
+    const long long lo = bnd[w], hi = bnd[w + 1];
+    bool ok = true;
+    for (long long j = 0; j < c; ++j) {
+      const long long x = buf[o + j];
+      ok &= x >= lo && x < hi && (j == 0 || x > buf[o + j - 1]);
+    }
+    if (!ok) atomicOr(bad, BAD_WINDOW);
+  }
+}
+
 // ----------------------------------------------------------------- K1 (CSR)
 // One warp per (input p, group of 128-window tiles); lane l owns windows
 // 4l..4l+3.  cut_w = lower bound of b_w in p's sorted toggles (slice_windows,

@@ -254,3 +254,33 @@ def test_config_c5_variants_match_oracle(oracle_lib, variant):
         assert np.array_equal(getattr(stats, f), ref[f]), f
     assert diag["discarded"] == int(a["discarded"].sum())
     assert diag["ic_filtered"] == int(a["ic_filtered"].sum())
+
+
+def test_c_abi_rejects_malformed_stimulus_on_device():
+    # gs_stim_create validates the uploaded stimulus with a device kernel
+    # (K0); malformed input is a ValueError naming the problem, as before
+    from paper_2203_06117_b200 import _native
+    docs, _ = load_golden("many_windows")
+    nl, lv, delays, waves, duration, b, stim = gen.load(docs, api)
+    dev = api.compile_design(lv, delays).device()
+    off, times, init = stim.pi_off.copy(), stim.pi_times.copy(), stim.pi_init.copy()
+    _native.Stimulus(dev, StimulusSet.from_csr(b, off, times, init))  # well formed
+    p = int(np.argmax(np.diff(off) >= 2))   # an input with two or more toggles
+    bad = times.copy()
+    bad[off[p] + 1] = bad[off[p]]           # repeated toggle time
+    with pytest.raises(ValueError, match="strictly increasing"):
+        _native.Stimulus(dev, StimulusSet.from_csr(b, off, bad, init))
+    win = StimulusSet(b, stim.buf.copy(), stim.offsets.copy(), stim.counts.copy(),
+                      stim.initials.copy(), stim.duration)
+    _native.Stimulus(dev, win)
+    i = int(np.argmax(win.counts.ravel() >= 1))
+    shifted = win.buf.copy()
+    shifted[win.offsets.ravel()[i]] = b[-1] + 5   # toggle past its window
+    with pytest.raises(ValueError, match="outside its window"):
+        _native.Stimulus(dev, StimulusSet(b, shifted, win.offsets, win.counts, win.initials,
+                                          win.duration))
+    cnt = win.counts.copy()
+    cnt.ravel()[i] = win.buf.size + 1                # region past the buffer
+    with pytest.raises(ValueError, match="out of range"):
+        _native.Stimulus(dev, StimulusSet(b, win.buf, win.offsets, cnt, win.initials,
+                                          win.duration))
