@@ -609,7 +609,7 @@ __device__ __forceinline__ void event_loop(
   unsigned dv = 0;
   TT dt = 0, t1w = 0;
   int w = -1;
-  bool has = false, more = ok;
+  bool has = false;
   unsigned cur[KM] = {}, end[KM] = {}, idx = 0, y = 0, y0 = 0, so = 0;
   TT nxt[KM] = {}, wlen = 0, t_last = 0, t_stored = 0;
   int cnt = 0, peak = 0, filt = 0, icf = 0, disc = 0;
@@ -640,44 +640,87 @@ __device__ __forceinline__ void event_loop(
     const TT add = (SMEM && sizeof(TT) == 4) ? (TT)0 : ic[p];  // staged = arrival time
     nxt[p] = q < end[p] ? in_at(p, q) + add : INF;
   };
-  while (true) {
-    if (!has && more) {
-      const unsigned nw = atomicAdd(&S.next, 1u);
-      if (nw < (unsigned)nwork) {
-        w = SMEM ? (int)S.work[nw] : (int)nw;
-        has = true;
-        cnt = peak = filt = disc = 0;
-        icf = (SMEM && MODE != MODE_STATS) ? (int)S.icfw[w] : 0;  // for record_arena
+  // take work item nw: window state, first transition of every pin
+  auto start = [&](unsigned nw) {
+    w = SMEM ? (int)S.work[nw] : (int)nw;
+    has = true;
+    cnt = peak = filt = disc = 0;
+    icf = (SMEM && MODE != MODE_STATS) ? (int)S.icfw[w] : 0;  // for record_arena
 #pragma unroll
-        for (int p = 0; p < kk; ++p) {
-          cur[p] = S.offs[p][w];
-          end[p] = SMEM ? (unsigned)S.fend[p][w] : S.offs[p][w + 1];
-          refresh(p);
-        }
-        idx = S.idx0[w];
-        y0 = y = lut_bit(lut, kk, D.lut_words, idx);
-        wlen = S.wlen[w];
-        so = S.ubo[w];
-        has_last = last_stored = false;
-        dv = y0;
-        dt = t1w = 0;
-      } else {
-        more = false;
-      }
+    for (int p = 0; p < kk; ++p) {
+      cur[p] = S.offs[p][w];
+      end[p] = SMEM ? (unsigned)S.fend[p][w] : S.offs[p][w + 1];
+      refresh(p);
     }
-    if (!__any_sync(0xffffffffu, has)) break;
+    idx = S.idx0[w];
+    y0 = y = lut_bit(lut, kk, D.lut_words, idx);
+    wlen = S.wlen[w];
+    so = S.ubo[w];
+    has_last = last_stored = false;
+    dv = y0;
+    dt = t1w = 0;
+  };
+  // window exhausted: flush the pending edge, record the window
+  auto finish = [&]() {
+    if (has_last && last_stored) {
+      out_at(cnt) = (TS)t_last;
+      ++cnt;
+      peak = max(peak, cnt);
+      t1w += dv ? t_last - dt : (TT)0;
+      dv ^= 1u;
+      dt = t_last;
+    }
+    if (PCT100) l_t1 += (long long)(t1w + (dv ? wlen - dt : (TT)0));
+    S.cnt[w] = (unsigned)cnt;
+    S.y0[w] = (unsigned char)y0;
+    l_filt += filt;
+    if (!SMEM) l_icf += icf;  // staged tiles: counted by the phase-1 filter
+    l_disc += disc;
+    record_arena<MODE, TS>(C, g, base_w + w, cnt, peak, filt, icf, disc, y0,
+                           [&](int j) { return out_at(j); });
+    has = false;
+  };
+  auto first_event = [&]() {
+    TT t = nxt[0];
+#pragma unroll
+    for (int p = 1; p < kk; ++p) t = min(t, nxt[p]);
+    return t;
+  };
+  // exhausted (or, read in place, empty) window: finish it and take work
+  // items until one has an event or the list is used up
+  volatile unsigned *next = &S.next;
+  TT tmin = INF;
+  auto refill = [&]() {
+    while (*next < (unsigned)nwork) {
+      if (has) finish();
+      const unsigned nw = atomicAdd(&S.next, 1u);
+      if (nw >= (unsigned)nwork) break;
+      start(nw);
+      tmin = first_event();
+      if (tmin != INF) break;
+    }
+  };
+  // Work items 0..31 go to lanes 0..31 (the shared counter starts past them);
+  // a lane whose window runs out while items remain finishes it and takes the
+  // next one inside the loop.  Once the list is used up, exhausted windows
+  // just stop, and are finished together after the loop, so the tail of the
+  // loop (few long windows still running) carries no finishing code.
+  if (ok && lane_id() < (unsigned)nwork) {
+    start(lane_id());
+    tmin = first_event();
+  }
+  if (!SMEM && ok && has && tmin == INF) refill();
+  while (true) {
+    const bool live = has && tmin != INF;
+    if (!__any_sync(0xffffffffu, live)) break;
 #ifdef GS_PROF
     {
-      const unsigned b = __ballot_sync(0xffffffffu, has);
+      const unsigned b = __ballot_sync(0xffffffffu, live);
       GS_PROF_ADD(PF_ITER, 1);
       GS_PROF_ADD(PF_BUSY_LANES, __popc(b));
     }
 #endif
-    if (!has) continue;
-    TT tmin = nxt[0];
-#pragma unroll
-    for (int p = 1; p < kk; ++p) tmin = min(tmin, nxt[p]);
-    if (SMEM || tmin != INF) {  // staged loop windows hold >= 3 transitions
+    if (live) {
       // multiple simultaneous inputs: consume every pin arriving at tmin, then
       // advance those pins to their next transition
       unsigned sw = 0;
@@ -698,7 +741,7 @@ __device__ __forceinline__ void event_loop(
           refresh(p);
         }
       }
-      // Output side (K:136-193), as selects rather than branches so the lanes
+    // Output side (K:136-193), as selects rather than branches so the lanes
       // of the warp stay converged: schedule the edge through the inertial
       // filter; cancel the pulse, or keep the previous edge and make this one
       // the pending edge (discarded when it lands at or past the window end).
@@ -755,33 +798,11 @@ __device__ __forceinline__ void event_loop(
       t_last = emit ? t_out : t_last;
       has_last = emit || (has_last && !cancel);
       y = chg ? ny : y;
-    }
-    // window exhausted (checked right after its last event, so finishing a
-    // window does not cost a loop iteration of its own): flush the pending
-    // edge, record the window
-    TT tn = nxt[0];
-#pragma unroll
-    for (int p = 1; p < kk; ++p) tn = min(tn, nxt[p]);
-    if (tn == INF) {
-      if (has_last && last_stored) {
-        out_at(cnt) = (TS)t_last;
-        ++cnt;
-        peak = max(peak, cnt);
-        t1w += dv ? t_last - dt : (TT)0;
-        dv ^= 1u;
-        dt = t_last;
-      }
-      if (PCT100) l_t1 += (long long)(t1w + (dv ? wlen - dt : (TT)0));
-      S.cnt[w] = (unsigned)cnt;
-      S.y0[w] = (unsigned char)y0;
-      l_filt += filt;
-      if (!SMEM) l_icf += icf;  // staged tiles: counted by the phase-1 filter
-      l_disc += disc;
-      record_arena<MODE, TS>(C, g, base_w + w, cnt, peak, filt, icf, disc, y0,
-                             [&](int j) { return out_at(j); });
-      has = false;
+      tmin = first_event();
+      if (tmin == INF) refill();
     }
   }
+  if (has) finish();
   acc_t1 += l_t1;
   acc_filt += l_filt;
   acc_icf += l_icf;
@@ -868,7 +889,7 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
     }
     st4(&S.wlen[wl], w4);
   }
-  if (lane == 0) S.next = 0;
+  if (lane == 0) S.next = kWarp;  // work items 0..31 start on lanes 0..31
   // Staging: fanin segments (UB words) then outputs (UB words) in the smem
   // slab when 2 * UB fits; otherwise inputs are read in place and outputs go
   // to this warp's region of the pool.
