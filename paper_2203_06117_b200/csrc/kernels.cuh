@@ -508,10 +508,10 @@ struct alignas(16) TileSmem {
   TS slab[kSlab];                  // staged fanin segments, then output staging
   // the item's condition tables (narrow kernels): arcs[(p << (KM-1) | row) * 2 + col]
   unsigned arcs[KM <= 4 ? KM * (1 << (KM - 1)) * 2 : 1];
-  // output delay by (switching pins, post-transition inputs, edge): the max
-  // over the switching arcs of the conditioned delay (K:139-151), tabulated
-  // once per gate so the event step does one lookup
-  unsigned dtab[KM <= 4 ? (1 << (2 * KM)) * 2 : 1];
+  // conditioned delay of pin p's arc by (p, post-transition inputs, edge)
+  // (K:139-151), tabulated once per gate so the event step does one lookup;
+  // simultaneous pins take the max over their entries
+  unsigned dtab[KM <= 4 ? KM * (1 << KM) * 2 : 1];
 
   // per-window arrays: rows 16-byte aligned so a lane's kWPL = 4 windows
   // move with one vector access (ld4 / st4)
@@ -575,6 +575,21 @@ __device__ __forceinline__ void record_arena(const ChunkDev &C, int g, int wr, i
   }
 }
 
+// dtab lookup for the switching pin set sw (non-empty): one entry for a single
+// pin; the max over the pins' entries when several switch at once (MSI)
+template <int K>
+__device__ __forceinline__ unsigned dtab_delay(const unsigned *dtab, unsigned sw, unsigned idx,
+                                               int col) {
+  const unsigned p = __ffs(sw) - 1;
+  unsigned d = dtab[(((p << K) | idx) << 1) | (unsigned)col];
+  if (sw & (sw - 1)) {
+#pragma unroll
+    for (int q = 1; q < K; ++q)
+      if ((sw >> q) & 1u) d = max(d, dtab[((((unsigned)q << K) | idx) << 1) | (unsigned)col]);
+  }
+  return d;
+}
+
 // output delay for the switching pin set sw and post-transition inputs idx
 template <typename TS, typename TT, int K>
 __device__ __forceinline__ TT event_delay(const DesignDev &D,
@@ -582,7 +597,7 @@ __device__ __forceinline__ TT event_delay(const DesignDev &D,
                                           const int *arc, int kk, unsigned sw, unsigned idx,
                                           int col) {
   if constexpr (K > 0 && K <= 4 && sizeof(TT) == 4) {
-    return (TT)S.dtab[(((sw << K) | idx) << 1) | (unsigned)col];
+    return dtab_delay<K>(S.dtab, sw, idx, col);
   } else {
     TT dly = 0;
     constexpr int KM = K > 0 ? K : kMaxK;
@@ -750,7 +765,7 @@ __device__ __forceinline__ void event_loop(
       const int col = ny ? 0 : 1;
       TT dly = 0;
       if constexpr (K > 0 && K <= 4 && sizeof(TT) == 4) {
-        dly = (TT)S.dtab[(((sw << K) | idx) << 1) | (unsigned)col];
+        dly = (TT)dtab_delay<K>(S.dtab, sw, idx, col);
       } else {
 #pragma unroll
         for (int p = 0; p < kk; ++p)
@@ -807,6 +822,43 @@ __device__ __forceinline__ void event_loop(
   acc_filt += l_filt;
   acc_icf += l_icf;
   acc_disc += l_disc;
+}
+
+// Interconnect inertial filter of pin p's staged segment, one lane's kWPL
+// windows: greedy removal of adjacent pairs narrower than d, compacting the
+// staged copy in place.  Same decisions as sim_span's lazy check
+// (_kernels.py:96-117): each one depends only on s[q], s[q+1] and the
+// positions are visited in the same order.  Sets fend[p][w]; returns the
+// removed pairs per window, 16 bits each.  Out of line: it only runs for the
+// few segments the cheap check flags, and inlined (unrolled per pin) it would
+// crowd the instruction cache of the hot path.
+template <typename TS, typename TT, int KM>
+__device__ __noinline__ unsigned long long pair_filter(TileSmem<TS, TT, KM> &S, int p,
+                                                       unsigned base, TT d, int wl) {
+  unsigned long long f = 0;
+#pragma unroll 1
+  for (int j = 0; j < kWPL; ++j) {
+    const unsigned a = base + S.offs[p][wl + j];
+    const unsigned b = base + S.offs[p][wl + j + 1];
+    unsigned e = b;
+    // the prefix before the first narrow pair stays where it is
+    unsigned i = a;
+    while (i + 1 < b && (TT)S.slab[i + 1] - (TT)S.slab[i] >= d) ++i;
+    if (i + 1 < b) {
+      unsigned o2 = i;
+      while (i < b) {
+        if (i + 1 < b && (TT)S.slab[i + 1] - (TT)S.slab[i] < d) {
+          i += 2;
+          f += 1ull << (16 * j);
+        } else {
+          S.slab[o2++] = S.slab[i++];
+        }
+      }
+      e = o2;
+    }
+    S.fend[p][wl + j] = (unsigned short)(e - base);
+  }
+  return f;
 }
 
 template <typename TS, typename TT, int MODE, int K, bool PCT100>
@@ -962,30 +1014,9 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
         st4(&S.fend[p][wl], e4);
         continue;
       }
+      const unsigned long long fp = pair_filter(S, p, inb_off[p], d, wl);
 #pragma unroll
-      for (int j = 0; j < kWPL; ++j) {
-        const unsigned a = inb_off[p] + S.offs[p][wl + j];
-        const unsigned b = inb_off[p] + S.offs[p][wl + j + 1];
-        unsigned e = b;
-        if (d > 0) {
-          // the prefix before the first narrow pair stays where it is
-          unsigned i = a;
-          while (i + 1 < b && (TT)S.slab[i + 1] - (TT)S.slab[i] >= d) ++i;
-          if (i + 1 < b) {
-            unsigned o2 = i;
-            while (i < b) {
-              if (i + 1 < b && (TT)S.slab[i + 1] - (TT)S.slab[i] < d) {
-                i += 2;
-                ++f[j];
-              } else {
-                S.slab[o2++] = S.slab[i++];
-              }
-            }
-            e = o2;
-          }
-        }
-        S.fend[p][wl + j] = (unsigned short)(e - inb_off[p]);
-      }
+      for (int j = 0; j < kWPL; ++j) f[j] += (unsigned)(fp >> (16 * j)) & 0xFFFFu;
     }
     st4(&S.icfw[wl], f);
 #pragma unroll
@@ -1236,16 +1267,11 @@ gate_eval(DesignDev D, ChunkDev C, LevelArgs A) {
       }
       __syncwarp();
       constexpr int KK = K > 0 ? K : 1;
-      for (int i = (int)lane; i < (1 << (2 * KK)) * 2; i += kWarp) {
-        const unsigned col = i & 1, id = (i >> 1) & ((1u << KK) - 1), sw = (unsigned)i >> (KK + 1);
-        unsigned dmax = 0;
-        for (int pp = 0; pp < KK; ++pp) {
-          if ((sw >> pp) & 1u) {
-            const unsigned row = (id & ((1u << pp) - 1u)) | ((id >> (pp + 1)) << pp);
-            dmax = max(dmax, S.arcs[((pp * R) + row) * 2 + col]);
-          }
-        }
-        S.dtab[i] = dmax;
+      for (int i = (int)lane; i < KK * (1 << KK) * 2; i += kWarp) {
+        const unsigned col = i & 1, id = (i >> 1) & ((1u << KK) - 1), pp = (unsigned)i >> (KK + 1);
+        // condition row: the other pins' values (pin pp's own bit removed)
+        const unsigned row = (id & ((1u << pp) - 1u)) | ((id >> (pp + 1)) << pp);
+        S.dtab[i] = S.arcs[((pp * R) + row) * 2 + col];
       }
       __syncwarp();
     }
