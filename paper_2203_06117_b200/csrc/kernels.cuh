@@ -525,6 +525,8 @@ struct alignas(16) TileSmem {
   alignas(16) unsigned short idx0[kTile];    // window-start input vector
   alignas(16) unsigned char y0[kTile];       // window-start output value
   unsigned char work[kTile];                 // windows left for the event loop
+  unsigned pin_inb[KM];                      // pin p's staged segment starts at slab[pin_inb[p]]
+  TT pin_icd[KM];                            // pin p's interconnect delay
   unsigned next;                             // dynamic window counter
 };
 
@@ -960,6 +962,7 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
       for (unsigned i = lane; i < tot[p]; i += kWarp)
         __pipeline_memcpy_async(&S.slab[o + i], src + i, sizeof(TS));
       inb_off[p] = o;
+      S.pin_inb[p] = o;
       o += tot[p];
     }
     __pipeline_commit();
@@ -982,9 +985,12 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
     unsigned f[kWPL];
 #pragma unroll
     for (int j = 0; j < kWPL; ++j) f[j] = 0;
-#pragma unroll
+    // (a pin loop, not unrolled: per-pin values come from smem, which keeps
+    // this code small for the instruction cache of the wide-fanin kernels)
+#pragma unroll 1
     for (int p = 0; p < kk; ++p) {
-      const TT d = ic[p];
+      const TT d = S.pin_icd[p];
+      const unsigned base = S.pin_inb[p];
       // Cheap exact check first: a lane's kWPL windows are one contiguous run
       // of the segment, so one pass over it (skipping the pairs that straddle
       // a window boundary) finds whether any pair is narrower than d.  Most
@@ -994,7 +1000,7 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
       if (d > 0) {
         unsigned bo[kWPL + 1];
 #pragma unroll
-        for (int j = 0; j <= kWPL; ++j) bo[j] = inb_off[p] + S.offs[p][wl + j];
+        for (int j = 0; j <= kWPL; ++j) bo[j] = base + S.offs[p][wl + j];
         if (bo[kWPL] > bo[0]) {
           TT prev = (TT)S.slab[bo[0]];
           for (unsigned i = bo[0] + 1; i < bo[kWPL]; ++i) {
@@ -1014,7 +1020,7 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
         st4(&S.fend[p][wl], e4);
         continue;
       }
-      const unsigned long long fp = pair_filter(S, p, inb_off[p], d, wl);
+      const unsigned long long fp = pair_filter(S, p, base, d, wl);
 #pragma unroll
       for (int j = 0; j < kWPL; ++j) f[j] += (unsigned)(fp >> (16 * j)) & 0xFFFFu;
     }
@@ -1257,6 +1263,7 @@ gate_eval(DesignDev D, ChunkDev C, LevelArgs A) {
       net[p] = __ldg(D.pin_net + pin0 + p);
       ic[p] = (TT)__ldg(D.pin_ic + pin0 + p);
       arc[p] = __ldg(D.pin_arc + pin0 + p);
+      S.pin_icd[p] = ic[p];
     }
     if (K > 0 && K <= 4 && sizeof(TT) == 4) {
       // condition tables of this gate -> smem: arcs[(p << (K-1) | row) * 2 + col]
