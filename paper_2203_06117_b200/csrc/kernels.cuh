@@ -63,7 +63,13 @@ constexpr int kTile = GS_TILE;              // windows per (gate, tile) work uni
 constexpr int kWPL = kTile / kWarp;         // windows per lane in the cooperative phases
 constexpr int kEvalWarps = 4;               // warps per K4 CTA
 constexpr int kEvalThreads = kEvalWarps * kWarp;
-constexpr int kSlab = 1024;                 // staged output timestamps per warp (smem)
+// staged words per warp (smem): as large as each fixed-k kernel's occupancy
+// allows (6 CTAs of 4 warps for k <= 2, 5 for k = 3, 4), so that few tiles
+// overflow to the in-place path
+template <int KM>
+__host__ __device__ constexpr int slab_words() {
+  return KM == 1 || KM == 2 ? 1280 : KM == 3 ? 1536 : KM == 4 ? 1152 : 1024;
+}
 constexpr int kMaxK = 16;                   // netlist.py:17 MAX_CELL_INPUTS
 constexpr long long kInf = LLONG_MAX;
 
@@ -505,7 +511,7 @@ __device__ __forceinline__ unsigned ld4_u8(const unsigned char *p) {  // 4 bytes
 
 template <typename TS, typename TT, int KM>
 struct alignas(16) TileSmem {
-  TS slab[kSlab];                  // staged fanin segments, then output staging
+  TS slab[slab_words<KM>()];       // staged fanin segments, then output staging
   // the item's condition tables (narrow kernels): arcs[(p << (KM-1) | row) * 2 + col]
   unsigned arcs[KM <= 4 ? KM * (1 << (KM - 1)) * 2 : 1];
   // conditioned delay of pin p's arc by (p, post-transition inputs, edge)
@@ -947,7 +953,7 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   // Staging: fanin segments (UB words) then outputs (UB words) in the smem
   // slab when 2 * UB fits; otherwise inputs are read in place and outputs go
   // to this warp's region of the pool.
-  const bool in_smem = 2 * UB <= (unsigned)kSlab;
+  const bool in_smem = 2 * UB <= (unsigned)slab_words<KM>();
   unsigned nwork = (unsigned)nact;  // windows for the event loop
   unsigned inb_off[KM];            // smem: pin p's tile segment starts at slab[inb_off[p]]
   const TS *inb_glob[KM];          // else: read in place

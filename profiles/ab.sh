@@ -2,6 +2,6 @@
 # HEAD build as libglsim_cuda_head.so vs the working-copy build, alternated.
 for i in 1 2; do
   for lib in libglsim_cuda_head.so libglsim_cuda.so; do
-    printf "%s " $lib; GLSIM_LIB=$lib python bench.py --steps 8 --warmup 3 --no-cpu-baseline --e2e-steps 1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step'],3))"
+    printf "%s " $lib; GLSIM_LIB=$lib timeout 300 python bench.py --steps 8 --warmup 3 --no-cpu-baseline --e2e-steps 1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step'],3))"
   done
 done

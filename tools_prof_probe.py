@@ -18,4 +18,5 @@ for i, n in enumerate(names):
     print(f"{n:16s} {v[i]/tot*100:5.1f}% of warp-cycles")
 print(f"tiles {v[8]}, slow(global) tiles {v[10]}, trivial windows {v[9]}, loop windows {v[7]}")
 print(f"loop iterations {v[4]}, avg busy lanes/iter {v[5]/max(v[4],1):.2f}, iters per tile {v[4]/max(v[8],1):.1f}")
+print(f"slow tile cycles {v[11]/tot*100:.1f}% of warp-cycles, avg UB {v[12]/max(v[10],1):.0f}")
 print(f"device ms {eng.timing()['ms_gate_eval']:.2f}")
