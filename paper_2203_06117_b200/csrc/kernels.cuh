@@ -621,7 +621,7 @@ __device__ __forceinline__ void event_loop(
     const DesignDev &D, const ChunkDev &C, int g, int kk, unsigned long long lut, const TT *ic,
     const int *arc, int pct, TileSmem<TS, TT, (K > 0 ? K : kMaxK)> &S,
     const typename std::conditional<SMEM, unsigned, const TS *>::type *inb, TS *stage,
-    unsigned stage_off, bool ok, int base_w, int nwork, long long &acc_t1,
+    bool ok, int base_w, int nwork, long long &acc_t1,
     long long &acc_filt, long long &acc_icf, long long &acc_disc) {
   constexpr int KM = K > 0 ? K : kMaxK;
   const TT INF = TimeTraits<TT>::inf();
@@ -641,10 +641,7 @@ __device__ __forceinline__ void event_loop(
     if constexpr (SMEM) return (TT)S.slab[inb[p] + q];
     else return (TT)__ldg(inb[p] + q);
   };
-  auto out_at = [&](int i) -> TS & {
-    if constexpr (SMEM) return S.slab[stage_off + so + i];
-    else return stage[so + i];
-  };
+  auto out_at = [&](int i) -> TS & { return stage[so + i]; };
   // next surviving transition of pin p at or after cur[p]: with smem staging
   // the interconnect pair filter was applied in phase 1; reading in place it
   // runs here, lazily, exactly as sim_span does (_kernels.py:96-117)
@@ -951,15 +948,21 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   }
   if (lane == 0) S.next = kWarp;  // work items 0..31 start on lanes 0..31
   // Staging: fanin segments (UB words) then outputs (UB words) in the smem
-  // slab when 2 * UB fits; otherwise inputs are read in place and outputs go
-  // to this warp's region of the pool.
-  const bool in_smem = 2 * UB <= (unsigned)slab_words<KM>();
+  // slab when 2 * UB fits; inputs only when UB fits (outputs then go to this
+  // warp's region of the pool); otherwise inputs are read in place as well.
+  const bool in_smem = UB <= (unsigned)slab_words<KM>();
+  const bool out_smem = 2 * UB <= (unsigned)slab_words<KM>();
   unsigned nwork = (unsigned)nact;  // windows for the event loop
   unsigned inb_off[KM];            // smem: pin p's tile segment starts at slab[inb_off[p]]
   const TS *inb_glob[KM];          // else: read in place
-  TS *stage;
+  TS *stage = S.slab + UB;
   bool ok = true;
-  if (in_smem) {
+  if (in_smem && !out_smem) {
+    const unsigned long long sb = region_alloc(C, R, UB);
+    ok = sb != ~0ull;
+    stage = data + (ok ? sb : 0ull);
+  }
+  if (in_smem && ok) {
     unsigned o = 0;
     // all pins' segments in flight at once (cp.async), one wait
 #pragma unroll
@@ -981,7 +984,6 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
         if (ic[p] != 0)
           for (unsigned i = lane; i < tot[p]; i += kWarp) S.slab[inb_off[p] + i] += (TS)ic[p];
     }
-    stage = S.slab + UB;
     __syncwarp();
     // interconnect inertial filter, applied once per (pin, window): greedy
     // removal of adjacent pairs narrower than the pin's delay, compacting the
@@ -1112,7 +1114,7 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
       const bool fl = e2 ? in2 : (c1 && !x2 && in1);             // ... and flushed
       const unsigned cnt = (st1 ? 1u : 0u) + (fl ? 1u : 0u);
       const TT f0 = st1 ? o1 : tp;
-      TS *st = S.slab + UB + S.ubo[w];
+      TS *st = stage + S.ubo[w];
       if (cnt >= 1) st[0] = (TS)f0;
       if (cnt == 2) st[1] = (TS)tp;
       const int disc = (c1 && !in1 ? 1 : 0) + (e2 && !in2 ? 1 : 0) - (x2 && !in1 ? 1 : 0);
@@ -1134,6 +1136,9 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
     }
     acc_filt += cf_filt;
     acc_disc += cf_disc;
+  } else if (in_smem) {  // pool full: the chunk is re-run; record empty windows meanwhile
+#pragma unroll
+    for (int j = 0; j < kWPL; ++j) S.cnt[wl + j] = 0;
   } else {
 #pragma unroll
     for (int p = 0; p < kk; ++p) inb_glob[p] = data + tb[p];
@@ -1161,11 +1166,11 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   // ---- phase 2: one lockstep loop (see event_loop)
   if (in_smem) {
     event_loop<TS, TT, MODE, K, PCT100, true>(D, C, g, kk, lut, ic, arc, pct, S, inb_off, stage,
-                                              UB, ok, base_w, (int)nwork, acc_t1, acc_filt,
+                                              ok, base_w, (int)nwork, acc_t1, acc_filt,
                                               acc_icf, acc_disc);
   } else {
     event_loop<TS, TT, MODE, K, PCT100, false>(D, C, g, kk, lut, ic, arc, pct, S, inb_glob,
-                                               stage, 0, ok, base_w, (int)nwork, acc_t1,
+                                               stage, ok, base_w, (int)nwork, acc_t1,
                                                acc_filt, acc_icf, acc_disc);
   }
   __syncwarp();
@@ -1205,7 +1210,7 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
       // continue in a loop
       if (wrote) {
         unsigned q = 0;
-        if (in_smem) {
+        if (out_smem) {
           const TS a0 = src[0], a1 = src[1];
           if (c[j] > 0) dst[0] = a0;
           if (c[j] > 1) dst[1] = a1;

@@ -284,3 +284,36 @@ def test_c_abi_rejects_malformed_stimulus_on_device():
     with pytest.raises(ValueError, match="out of range"):
         _native.Stimulus(dev, StimulusSet(b, win.buf, win.offsets, cnt, win.initials,
                                           win.duration))
+
+
+# staged words per warp of the fixed-k kernels (kernels.cuh slab_words); the
+# generic k <= 16 kernel stages 1024
+SLAB = {1: 1280, 2: 1280, 3: 1536, 4: 1152}
+
+
+@pytest.mark.parametrize("seed,max_toggles", [(1, 250), (2, 700), (3, 1500), (4, 4000)])
+def test_busy_tiles_take_every_staging_path(oracle_lib, seed, max_toggles):
+    # Tiles with many fanin toggles leave the fully staged fast path: inputs in
+    # shared memory with outputs staged in the pool (UB <= slab < 2 UB), or both
+    # read and staged in global memory (UB > slab).  All must agree with the
+    # oracle; the instances are checked to actually reach those paths.
+    docs = gen.make_docs(9100 + seed, n_gates=240, n_pis=6, windows=6, duration_ps=60_000,
+                         max_toggles=max_toggles, max_delay=1_500, max_levels=5)
+    nl, lv, delays, stim, arena, diag, stats = gpu_run(docs)
+    waves = gen.load(docs, api)[3]
+    d, st, oa, os_ = oracle_lib.simulate(lv, delays, gen.oracle_inputs(nl, waves),
+                                         stim.boundaries, threads=4)
+    for f in ("buf", "offsets", "caps", "counts", "initials", "filtered", "ic_filtered",
+              "discarded"):
+        assert np.array_equal(getattr(arena, f), oa[f]), f"arena.{f}"
+    for f in ("t0", "t1", "tc", "ig"):
+        assert np.array_equal(getattr(stats, f), os_[f]), f
+    # fanin toggles UB of each gate's (single, 6-window) tile -> staging path
+    m = api.compile_design(lv, delays)
+    net_tc = np.concatenate([stim.counts.sum(axis=1), arena.counts.sum(axis=1)])
+    ub = np.array([net_tc[m.pin_net[m.pin_off[i]:m.pin_off[i + 1]]].sum()
+                   for i in range(nl.num_gates)])
+    slab = np.array([SLAB.get(int(x), 1024) for x in np.diff(m.pin_off)])
+    hybrid = int(((ub <= slab) & (2 * ub > slab)).sum())
+    glob = int((ub > slab).sum())
+    assert hybrid + glob > 0, "instance never leaves the fully staged path"
