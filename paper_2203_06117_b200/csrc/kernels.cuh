@@ -514,10 +514,12 @@ struct alignas(16) TileSmem {
   TS slab[slab_words<KM>()];       // staged fanin segments, then output staging
   // the item's condition tables (narrow kernels): arcs[(p << (KM-1) | row) * 2 + col]
   unsigned arcs[KM <= 4 ? KM * (1 << (KM - 1)) * 2 : 1];
-  // conditioned delay of pin p's arc by (p, post-transition inputs, edge)
-  // (K:139-151), tabulated once per gate so the event step does one lookup;
-  // simultaneous pins take the max over their entries
-  unsigned dtab[KM <= 4 ? KM * (1 << KM) * 2 : 1];
+  // output delay tabulated once per gate so the event step does one lookup:
+  // k <= 2, by (switching pin set, post-transition inputs, edge) -- the max
+  // over the switching arcs of the conditioned delay (K:139-151); k = 3, 4 by
+  // (single pin, inputs, edge), simultaneous pins taking the max of their
+  // entries (the full 3- and 4-pin tables would cost an SM a CTA)
+  unsigned dtab[KM <= 2 ? (1 << (2 * KM)) * 2 : KM <= 4 ? KM * (1 << KM) * 2 : 1];
 
   // per-window arrays: rows 16-byte aligned so a lane's kWPL = 4 windows
   // move with one vector access (ld4 / st4)
@@ -588,6 +590,7 @@ __device__ __forceinline__ void record_arena(const ChunkDev &C, int g, int wr, i
 template <int K>
 __device__ __forceinline__ unsigned dtab_delay(const unsigned *dtab, unsigned sw, unsigned idx,
                                                int col) {
+  if constexpr (K <= 2) return dtab[(((sw << K) | idx) << 1) | (unsigned)col];
   const unsigned p = __ffs(sw) - 1;
   unsigned d = dtab[(((p << K) | idx) << 1) | (unsigned)col];
   if (sw & (sw - 1)) {
@@ -1285,11 +1288,23 @@ gate_eval(DesignDev D, ChunkDev C, LevelArgs A) {
       }
       __syncwarp();
       constexpr int KK = K > 0 ? K : 1;
-      for (int i = (int)lane; i < KK * (1 << KK) * 2; i += kWarp) {
-        const unsigned col = i & 1, id = (i >> 1) & ((1u << KK) - 1), pp = (unsigned)i >> (KK + 1);
-        // condition row: the other pins' values (pin pp's own bit removed)
-        const unsigned row = (id & ((1u << pp) - 1u)) | ((id >> (pp + 1)) << pp);
-        S.dtab[i] = S.arcs[((pp * R) + row) * 2 + col];
+      // condition row of pin pp: the other pins' values (pp's own bit removed)
+      auto row_of = [](unsigned id, unsigned pp) {
+        return (id & ((1u << pp) - 1u)) | ((id >> (pp + 1)) << pp);
+      };
+      if constexpr (KK <= 2) {
+        for (int i = (int)lane; i < (1 << (2 * KK)) * 2; i += kWarp) {
+          const unsigned col = i & 1, id = (i >> 1) & ((1u << KK) - 1), sw = (unsigned)i >> (KK + 1);
+          unsigned dmax = 0;
+          for (unsigned pp = 0; pp < (unsigned)KK; ++pp)
+            if ((sw >> pp) & 1u) dmax = max(dmax, S.arcs[((pp * R) + row_of(id, pp)) * 2 + col]);
+          S.dtab[i] = dmax;
+        }
+      } else {
+        for (int i = (int)lane; i < KK * (1 << KK) * 2; i += kWarp) {
+          const unsigned col = i & 1, id = (i >> 1) & ((1u << KK) - 1), pp = (unsigned)i >> (KK + 1);
+          S.dtab[i] = S.arcs[((pp * R) + row_of(id, pp)) * 2 + col];
+        }
       }
       __syncwarp();
     }
