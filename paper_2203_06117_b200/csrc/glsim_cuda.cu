@@ -61,6 +61,34 @@ int upload(T **p, const T *src, size_t n) {
   return GS_OK;
 }
 
+// Stimulus buffers come from the device's stream-ordered pool, kept warm (no
+// release to the OS at synchronisation), so a stimulus uploaded every step --
+// the end-to-end path -- does not pay cudaMalloc / cudaFree each time.
+int pool_ready(int dev) {
+  static bool done[64] = {};
+  if (dev < 0 || dev >= 64 || done[dev]) return GS_OK;
+  cudaMemPool_t pool;
+  CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+  unsigned long long thr = ~0ull;
+  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  done[dev] = true;
+  return GS_OK;
+}
+
+template <typename T>
+int upload_pooled(T **p, const T *src, size_t n) {
+  *p = nullptr;
+  CK(cudaMallocAsync((void **)p, (n ? n : 1) * sizeof(T), (cudaStream_t)0));
+  if (n) CK(cudaMemcpy(*p, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  return GS_OK;
+}
+
+template <typename T>
+void dfree_pooled(T *&p) {
+  if (p) cudaFreeAsync((void *)p, (cudaStream_t)0);
+  p = nullptr;
+}
+
 // run a validation kernel that ORs flags into a device int; return the flags
 template <typename F>
 int device_check(int *flags, F launch) {
@@ -284,8 +312,10 @@ struct gs_stim {
     return S;
   }
   void release() {
-    dfree(bnd); dfree(pi_off); dfree(pi_times); dfree(buf); dfree(offsets); dfree(counts);
-    dfree(pi_init); dfree(initials);
+    // engine streams may still read the stimulus: drain the device first
+    cudaDeviceSynchronize();
+    dfree_pooled(bnd); dfree_pooled(pi_off); dfree_pooled(pi_times); dfree_pooled(buf);
+    dfree_pooled(offsets); dfree_pooled(counts); dfree_pooled(pi_init); dfree_pooled(initials);
   }
 };
 
@@ -307,7 +337,8 @@ static int stim_build(gs_design *D, const gs_stim_desc *s, gs_stim *S) {
   S->max_wlen = maxlen;
   S->csr = s->pi_off != nullptr;
   TRY(use_device(D->device));
-  TRY(upload(&S->bnd, (const long long *)s->boundaries, S->W + 1));
+  TRY(pool_ready(D->device));
+  TRY(upload_pooled(&S->bnd, (const long long *)s->boundaries, S->W + 1));
   const int64_t P = S->P, W = S->W;
   if (S->csr) {
     if (!s->pi_times || !s->pi_init) return fail(GS_ERR_ARG, "incomplete CSR stimulus");
@@ -315,9 +346,9 @@ static int stim_build(gs_design *D, const gs_stim_desc *s, gs_stim *S) {
     for (int64_t p = 0; p < P; ++p)
       if (s->pi_off[p + 1] < s->pi_off[p]) return fail(GS_ERR_ARG, "pi_off not monotone");
     S->n_toggles = s->pi_off[P];
-    TRY(upload(&S->pi_off, (const long long *)s->pi_off, P + 1));
-    TRY(upload(&S->pi_times, (const long long *)s->pi_times, S->n_toggles));
-    TRY(upload(&S->pi_init, s->pi_init, P));
+    TRY(upload_pooled(&S->pi_off, (const long long *)s->pi_off, P + 1));
+    TRY(upload_pooled(&S->pi_times, (const long long *)s->pi_times, S->n_toggles));
+    TRY(upload_pooled(&S->pi_init, s->pi_init, P));
     int bad = 0;
     TRY(device_check(&bad, [&](int *flag) {
       stim_check_csr<<<std::max<int64_t>(1, std::min<int64_t>((P + 7) / 8, 4096)), 256>>>(
@@ -328,10 +359,10 @@ static int stim_build(gs_design *D, const gs_stim_desc *s, gs_stim *S) {
     if (!s->buf && s->n_buf) return fail(GS_ERR_ARG, "missing stimulus buffer");
     if (!s->offsets || !s->counts || !s->initials) return fail(GS_ERR_ARG, "incomplete windowed stimulus");
     S->n_toggles = s->n_buf;
-    TRY(upload(&S->buf, (const long long *)s->buf, s->n_buf));
-    TRY(upload(&S->offsets, (const long long *)s->offsets, P * W));
-    TRY(upload(&S->counts, (const long long *)s->counts, P * W));
-    TRY(upload(&S->initials, s->initials, P * W));
+    TRY(upload_pooled(&S->buf, (const long long *)s->buf, s->n_buf));
+    TRY(upload_pooled(&S->offsets, (const long long *)s->offsets, P * W));
+    TRY(upload_pooled(&S->counts, (const long long *)s->counts, P * W));
+    TRY(upload_pooled(&S->initials, s->initials, P * W));
     int bad = 0;
     TRY(device_check(&bad, [&](int *flag) {
       stim_check_win<<<(int)std::max<int64_t>(1, std::min<int64_t>((P * W + 255) / 256, 4096)),
