@@ -32,12 +32,17 @@ typedef enum gs_status {
   GS_ERR_CUDA = 2,        /* CUDA runtime failure              -> RuntimeError      */
   GS_ERR_NODEVICE = 3,    /* no CUDA device visible            -> RuntimeError      */
   GS_ERR_CAPACITY = 4,    /* device memory cannot hold one tile-> CapacityError     */
-  GS_ERR_CONSISTENCY = 5  /* device-side invariant violated    -> ConsistencyError  */
+  GS_ERR_CONSISTENCY = 5, /* device-side invariant violated    -> ConsistencyError  */
+  GS_ERR_PARSE = 6,       /* malformed document (line in gs_last_error_line) -> ParseError */
+  GS_ERR_SEMANTIC = 7,    /* document breaks a design contract -> SemanticError     */
+  GS_ERR_UNSUPPORTED = 8  /* input outside the native reader's byte-exact subset:
+                             the caller uses its own (Python) reader            */
 } gs_status;
 
 typedef struct gs_design gs_design;
 typedef struct gs_stim gs_stim;
 typedef struct gs_engine gs_engine;
+typedef struct gs_vcd gs_vcd;
 
 /* Flat design, exactly the arrays of reference CompiledDesign
  * (pkg/src/glsim/simcore.py:203-272) plus the levelization
@@ -179,6 +184,26 @@ int gs_dwell_sweep(int64_t num_nets, const uint8_t *net_kind, const int64_t *net
  * net; vals_out is [num_nets, W] uint8, rows < P copied from stim_init [P, W]. */
 int gs_init_values(const gs_design_desc *desc, const uint8_t *stim_init, int64_t num_windows,
                    uint8_t *vals_out);
+
+/* ---- stimulus document reader (host): the format immediately upstream of
+ * the path ------------------------------------------------ */
+
+/* parse_vcd (pkg/src/glsim/waveform.py:101-198): read a VCD document into
+ * per-input CSR waveforms for the inputs named pi_names[0..num_pis) (the
+ * netlist's primary inputs, in order) -- the form gs_stim_create takes.  On
+ * GS_ERR_PARSE / GS_ERR_SEMANTIC gs_last_error() holds the reference's
+ * message and gs_last_error_line() the 1-based line of a parse error.
+ * GS_ERR_UNSUPPORTED (non-ASCII text, Unicode separators, time values beyond
+ * int64): nothing was read; use the reference-semantics reader. */
+int gs_vcd_parse(const char *text, int64_t len, const char *const *pi_names, int64_t num_pis,
+                 gs_vcd **out);
+/* sizes of a parsed document: total toggles and the last time mark (fs) */
+int gs_vcd_sizes(const gs_vcd *v, int64_t *num_toggles, int64_t *duration);
+/* copy out pi_off [num_pis+1], pi_times [num_toggles], pi_init [num_pis] */
+int gs_vcd_copy(const gs_vcd *v, int64_t *pi_off, int64_t *pi_times, uint8_t *pi_init);
+int gs_vcd_destroy(gs_vcd *v);
+/* 1-based line of the last GS_ERR_PARSE (0 if none) */
+int64_t gs_last_error_line(void);
 
 #ifdef __cplusplus
 }

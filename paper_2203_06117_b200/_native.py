@@ -18,7 +18,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_NAME = "libglsim_cuda.so"
 LIB_PATH = os.path.join(_HERE, os.environ.get("GLSIM_LIB", LIB_NAME))
 
-GS_OK, GS_ERR_ARG, GS_ERR_CUDA, GS_ERR_NODEVICE, GS_ERR_CAPACITY, GS_ERR_CONSISTENCY = range(6)
+(GS_OK, GS_ERR_ARG, GS_ERR_CUDA, GS_ERR_NODEVICE, GS_ERR_CAPACITY, GS_ERR_CONSISTENCY,
+ GS_ERR_PARSE, GS_ERR_SEMANTIC, GS_ERR_UNSUPPORTED) = range(9)
 
 _i64p = C.POINTER(C.c_int64)
 _u8p = C.POINTER(C.c_uint8)
@@ -79,6 +80,12 @@ SIGNATURES = {
                                  C.c_int64, C.c_int64, _i64p, C.c_int64, C.c_int64, C.c_int64,
                                  _i64p, _i64p, _i64p]),
     "gs_init_values": (C.c_int, [C.POINTER(DesignDesc), _u8p, C.c_int64, _u8p]),
+    "gs_vcd_parse": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(C.c_char_p), C.c_int64,
+                               C.POINTER(C.c_void_p)]),
+    "gs_vcd_sizes": (C.c_int, [C.c_void_p, _i64p, _i64p]),
+    "gs_vcd_copy": (C.c_int, [C.c_void_p, _i64p, _i64p, _u8p]),
+    "gs_vcd_destroy": (C.c_int, [C.c_void_p]),
+    "gs_last_error_line": (C.c_int64, []),
 }
 
 _lib = None
@@ -113,6 +120,48 @@ def _check(rc):
     if rc == GS_ERR_ARG:
         raise ValueError(msg)
     raise RuntimeError(f"libglsim_cuda: {msg}")
+
+
+def vcd_parse(text, pi_names, path=None):
+    """Native VCD reader (``gs_vcd_parse``): -> ``(pi_off, pi_times, pi_init,
+    duration)``, or None when the library is not built or the text is outside
+    the native reader's byte-exact subset (the caller then uses the Python
+    reader).  Raises the reference's ParseError / SemanticError."""
+    from .errors import ParseError, SemanticError
+    try:
+        lib = load()
+    except RuntimeError:
+        return None
+    try:
+        raw = text.encode("ascii") if isinstance(text, str) else bytes(text)
+    except UnicodeEncodeError:
+        return None
+    names = [n.encode("ascii", errors="surrogateescape") if n.isascii() else None
+             for n in pi_names]
+    if any(n is None for n in names):
+        return None
+    arr = (C.c_char_p * max(1, len(names)))(*names)
+    h = C.c_void_p()
+    rc = lib.gs_vcd_parse(raw, len(raw), arr, len(names), C.byref(h))
+    if rc == GS_ERR_UNSUPPORTED:
+        return None
+    if rc in (GS_ERR_PARSE, GS_ERR_SEMANTIC):
+        msg = (lib.gs_last_error() or b"").decode()
+        if rc == GS_ERR_PARSE:
+            raise ParseError(msg, path, int(lib.gs_last_error_line()))
+        raise SemanticError(msg)
+    _check(rc)
+    try:
+        n, dur = C.c_int64(), C.c_int64()
+        _check(lib.gs_vcd_sizes(h, C.byref(n), C.byref(dur)))
+        P = len(names)
+        pi_off = np.empty(P + 1, dtype=np.int64)
+        pi_times = np.empty(n.value, dtype=np.int64)
+        pi_init = np.empty(P, dtype=np.uint8)
+        _check(lib.gs_vcd_copy(h, _p64(pi_off), _p64(pi_times), _p8(pi_init)))
+    finally:
+        lib.gs_vcd_destroy(h)
+    return pi_off, pi_times, pi_init, int(dur.value)
 
 
 def _p64(a):

@@ -12,15 +12,18 @@
 
 #include "glsim_cuda.h"
 #include "kernels.cuh"
+#include "vcd_reader.h"
 
 using namespace gs;
 
 namespace {
 
 thread_local std::string g_err;
+thread_local int64_t g_err_line = 0;
 
 int fail(int code, const std::string &msg) {
   g_err = msg;
+  g_err_line = 0;
   return code;
 }
 
@@ -837,6 +840,8 @@ int gs_version(void) { return 1; }
 
 const char *gs_last_error(void) { return g_err.c_str(); }
 
+int64_t gs_last_error_line(void) { return g_err_line; }
+
 int gs_device_count(int *count) {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
@@ -1101,6 +1106,65 @@ int gs_init_values(const gs_design_desc *desc, const uint8_t *stim_init, int64_t
   dfree(vals);
   D.release();
   return rc;
+}
+
+// ---- VCD reader
+
+}  // extern "C"
+
+struct gs_vcd {
+  gsvcd::Result r;
+};
+
+extern "C" {
+
+int gs_vcd_parse(const char *text, int64_t len, const char *const *pi_names, int64_t num_pis,
+                 gs_vcd **out) {
+  if (!out || (len > 0 && !text) || num_pis < 0 || (num_pis > 0 && !pi_names))
+    return fail(GS_ERR_ARG, "null VCD text, input names or output handle");
+  if (num_pis > INT32_MAX) return fail(GS_ERR_ARG, "too many inputs");
+  *out = nullptr;
+  std::vector<std::string> names;
+  names.reserve((size_t)num_pis);
+  for (int64_t i = 0; i < num_pis; ++i) {
+    if (!pi_names[i]) return fail(GS_ERR_ARG, "null input name");
+    names.emplace_back(pi_names[i]);
+  }
+  gs_vcd *v = new gs_vcd();
+  const gsvcd::Status st = gsvcd::parse(text, len, names, v->r);
+  if (st != gsvcd::VCD_OK) {
+    const std::string msg = v->r.msg;
+    const int64_t line = v->r.line;
+    delete v;
+    if (st == gsvcd::VCD_FALLBACK)
+      return fail(GS_ERR_UNSUPPORTED, "VCD text outside the native reader's subset");
+    const int rc = fail(st == gsvcd::VCD_PARSE ? GS_ERR_PARSE : GS_ERR_SEMANTIC, msg);
+    g_err_line = st == gsvcd::VCD_PARSE ? line : 0;
+    return rc;
+  }
+  *out = v;
+  return GS_OK;
+}
+
+int gs_vcd_sizes(const gs_vcd *v, int64_t *num_toggles, int64_t *duration) {
+  if (!v || !num_toggles || !duration) return fail(GS_ERR_ARG, "null argument");
+  *num_toggles = (int64_t)v->r.pi_times.size();
+  *duration = v->r.duration;
+  return GS_OK;
+}
+
+int gs_vcd_copy(const gs_vcd *v, int64_t *pi_off, int64_t *pi_times, uint8_t *pi_init) {
+  if (!v || !pi_off || (!pi_times && !v->r.pi_times.empty()) || (!pi_init && !v->r.pi_init.empty()))
+    return fail(GS_ERR_ARG, "null argument");
+  std::copy(v->r.pi_off.begin(), v->r.pi_off.end(), pi_off);
+  std::copy(v->r.pi_times.begin(), v->r.pi_times.end(), pi_times);
+  std::copy(v->r.pi_init.begin(), v->r.pi_init.end(), pi_init);
+  return GS_OK;
+}
+
+int gs_vcd_destroy(gs_vcd *v) {
+  delete v;
+  return GS_OK;
 }
 
 }  // extern "C"
