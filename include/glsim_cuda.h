@@ -205,6 +205,20 @@ int gs_vcd_destroy(gs_vcd *v);
 /* 1-based line of the last GS_ERR_PARSE (0 if none) */
 int64_t gs_last_error_line(void);
 
+/* ---- activity report writer (host): the format immediately downstream of
+ * the path ------------------------------------------------ */
+
+/* write_saif (pkg/src/glsim/report.py:94-131): the byte-exact flat SAIF text
+ * for num_nets nets.  Net names are UTF-8, concatenated in `names` with
+ * name_off [num_nets+1] byte offsets; '[', ']', '/' and '\' are escaped with
+ * a backslash.  t0/t1/tc/ig [num_nets] (ig only if include_ig).  Writes at
+ * most out_cap bytes to `out` and the text length to *out_len; GS_ERR_ARG if
+ * out_cap is too small (*out_len then holds the size needed). */
+int gs_saif_format(const char *names, const int64_t *name_off, int64_t num_nets,
+                   const int64_t *t0, const int64_t *t1, const int64_t *tc, const int64_t *ig,
+                   int64_t duration, const char *design_name, const char *saif_version,
+                   int include_ig, char *out, int64_t out_cap, int64_t *out_len);
+
 #ifdef __cplusplus
 }
 #endif

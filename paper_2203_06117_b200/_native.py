@@ -86,6 +86,9 @@ SIGNATURES = {
     "gs_vcd_copy": (C.c_int, [C.c_void_p, _i64p, _i64p, _u8p]),
     "gs_vcd_destroy": (C.c_int, [C.c_void_p]),
     "gs_last_error_line": (C.c_int64, []),
+    "gs_saif_format": (C.c_int, [C.c_char_p, _i64p, C.c_int64, _i64p, _i64p, _i64p, _i64p,
+                                 C.c_int64, C.c_char_p, C.c_char_p, C.c_int, C.c_char_p,
+                                 C.c_int64, _i64p]),
 }
 
 _lib = None
@@ -162,6 +165,36 @@ def vcd_parse(text, pi_names, path=None):
     finally:
         lib.gs_vcd_destroy(h)
     return pi_off, pi_times, pi_init, int(dur.value)
+
+
+def saif_format(net_names, t0, t1, tc, ig, duration, design_name, version, include_ig):
+    """Native SAIF text (``gs_saif_format``), or None if the library is not
+    built (the caller then formats in Python)."""
+    try:
+        lib = load()
+    except RuntimeError:
+        return None
+    names = list(net_names)
+    joined = "".join(names)
+    lens = np.fromiter(map(len, names), dtype=np.int64, count=len(names))
+    if joined.isascii():  # one encode; byte offsets = character offsets
+        blob = joined.encode("ascii")
+    else:
+        enc = [n.encode("utf-8", errors="surrogatepass") for n in names]
+        lens = np.fromiter(map(len, enc), dtype=np.int64, count=len(enc))
+        blob = b"".join(enc)
+    off = np.zeros(len(names) + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    arrs = [_c64(a) for a in (t0, t1, tc, ig)]
+    dname = str(design_name).encode("utf-8", errors="surrogatepass")
+    args = (blob, _p64(off), len(names), *[_p64(a) for a in arrs], int(duration), dname,
+            version.encode(), int(bool(include_ig)))
+    need = C.c_int64()
+    lib.gs_saif_format(*args, None, 0, C.byref(need))
+    buf = np.empty(need.value, dtype=np.uint8)
+    n = C.c_int64()
+    _check(lib.gs_saif_format(*args, buf.ctypes.data_as(C.c_char_p), need.value, C.byref(n)))
+    return buf[:n.value].tobytes().decode("utf-8", errors="surrogatepass")
 
 
 def _p64(a):

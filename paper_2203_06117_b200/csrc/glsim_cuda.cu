@@ -5,6 +5,7 @@
 // then one K4 launch per logic level (the level barrier), all on one stream,
 // and synchronizes once at the chunk end to check the device-side flags.
 #include <algorithm>
+#include <charconv>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -1164,6 +1165,63 @@ int gs_vcd_copy(const gs_vcd *v, int64_t *pi_off, int64_t *pi_times, uint8_t *pi
 
 int gs_vcd_destroy(gs_vcd *v) {
   delete v;
+  return GS_OK;
+}
+
+// ---- SAIF writer
+
+int gs_saif_format(const char *names, const int64_t *name_off, int64_t num_nets,
+                   const int64_t *t0, const int64_t *t1, const int64_t *tc, const int64_t *ig,
+                   int64_t duration, const char *design_name, const char *saif_version,
+                   int include_ig, char *out, int64_t out_cap, int64_t *out_len) {
+  if (!out_len || !design_name || !saif_version || num_nets < 0 ||
+      (num_nets > 0 && (!names || !name_off || !t0 || !t1 || !tc || (include_ig && !ig))))
+    return fail(GS_ERR_ARG, "null SAIF writer argument");
+  std::string head;
+  head += "(SAIFILE\n  (SAIFVERSION \"";
+  head += saif_version;
+  head += "\")\n  (DIRECTION \"backward\")\n  (DESIGN \"";
+  head += design_name;
+  head += "\")\n  (TIMESCALE 1 fs)\n  (DURATION ";
+  head += std::to_string(duration);
+  head += ")\n  (INSTANCE ";
+  head += design_name;
+  head += "\n    (NET\n";
+  static const char tail[] = "    )\n  )\n)\n";
+  // size: every byte of a name may double; 20 digits + sign per number
+  int64_t need = (int64_t)head.size() + (int64_t)sizeof(tail) - 1;
+  for (int64_t i = 0; i < num_nets; ++i)
+    need += 2 * (name_off[i + 1] - name_off[i]) + 128 + 4 * 21;
+  if (!out || out_cap < need) {
+    *out_len = need;
+    return fail(GS_ERR_ARG, "SAIF output buffer too small");
+  }
+  char *p = out;
+  auto put = [&](const char *s, size_t n) { memcpy(p, s, n); p += n; };
+  auto lit = [&](const char *s) { put(s, strlen(s)); };
+  auto num = [&](int64_t v) { p = std::to_chars(p, p + 21, (long long)v).ptr; };
+  put(head.data(), head.size());
+  for (int64_t i = 0; i < num_nets; ++i) {
+    lit("      (");
+    for (int64_t j = name_off[i]; j < name_off[i + 1]; ++j) {
+      const char c = names[j];
+      if (c == '[' || c == ']' || c == '/' || c == '\\') *p++ = '\\';
+      *p++ = c;
+    }
+    lit("\n        (T0 ");
+    num(t0[i]);
+    lit(") (T1 ");
+    num(t1[i]);
+    lit(") (TX 0)\n        (TC ");
+    num(tc[i]);
+    if (include_ig) {
+      lit(") (IG ");
+      num(ig[i]);
+    }
+    lit(")\n      )\n");
+  }
+  put(tail, sizeof(tail) - 1);
+  *out_len = p - out;
   return GS_OK;
 }
 
