@@ -1,6 +1,7 @@
-"""Debug probe: per-phase cycle split of K4 on C2 (needs a -DGS_PROF build)."""
+"""Dev probe: per-phase cycle split of K4 on C2 (GS_PROF build: python -c "import __graft_entry__ as g; g.build_native(force=True, out='paper_2203_06117_b200/libglsim_cuda_prof.so', defines=['GS_PROF'])")."""
 import ctypes as C, os, sys
 import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ.setdefault("GLSIM_LIB", "libglsim_cuda_prof.so")
 from paper_2203_06117_b200 import synth, _native
 cfg = synth.config("C2")
