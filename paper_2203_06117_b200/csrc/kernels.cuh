@@ -16,18 +16,24 @@
 //      windows (reference StimulusSet.build + slice_windows, waveform.py:49-63,
 //      243-265), fused with the input nets' dwell/toggle sums (dwell_sweep,
 //      _kernels.py:254-295, PI rows).
-//   K4 gate_eval : one warp = one gate x one 128-window tile, in three phases:
+//   K4 gate_eval : one warp = one gate x one 128-window tile:
 //      (1) cooperative: coalesced loads of the fanin counts / bases / start
 //          bits, warp scans -> per-window fanin offsets, window-start input
 //          vectors (init_values, _kernels.py:213-231) and the per-window output
-//          bound (level_ub, _kernels.py:234-251) staged in shared memory;
-//      (2) one lockstep loop in which every lane with a window executes the
-//          same Algo. 1 event step of sim_span (_kernels.py:94-210); a lane
-//          whose window is exhausted pulls the next one from a shared counter,
-//          so busy windows do not leave the other lanes idle;
-//      (3) cooperative compaction: warp scan of the stored counts, one region
+//          bound (level_ub, _kernels.py:234-251) in shared memory; the fanin
+//          segments staged into the warp's smem slab (cp.async) and the
+//          interconnect pair filter applied to them once;
+//      (2) windows with <= 2 surviving input transitions: Algo. 1 in closed
+//          form, one window per lane per round;
+//      (3) the rest: one lockstep event loop in which every lane with a window
+//          executes the same Algo. 1 event step of sim_span
+//          (_kernels.py:94-210); a lane whose window runs out takes the next
+//          one from a shared counter;
+//      (4) cooperative compaction: warp scan of the stored counts, one region
 //          allocation, copy out of the staging area fused with the dwell /
 //          toggle reduction (dwell_sweep, gate rows).
+//      Tiles whose fanin toggles overflow the slab stage only their inputs
+//      in smem (outputs in the pool), or read everything in place.
 //   K6 dwell_arena : dwell_sweep over a host-provided arena (compute_stats).
 //   K2 zero_delay_level : init_values seam (one level, thread per gate-window).
 #pragma once
