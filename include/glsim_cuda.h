@@ -205,6 +205,37 @@ int gs_vcd_destroy(gs_vcd *v);
 /* 1-based line of the last GS_ERR_PARSE (0 if none) */
 int64_t gs_last_error_line(void);
 
+/* parse_sdf (pkg/src/glsim/sdf.py:229-503): read an SDF document into the
+ * flat delay arrays of the design -- arc_rows [R][2] (rise, fall per
+ * condition row; gates in order, each gate's pins in order, 2^(k-1) rows per
+ * pin: exactly gs_design_desc.arc_rows) and pin_ic [sum k] -- for the netlist
+ * described below.  corner: 0 min, 1 typ, 2 max.  Skipped constructs produce
+ * the reference's warnings (gs_sdf_warning).  Errors as gs_vcd_parse
+ * (gs_last_error_line / gs_last_error_col for GS_ERR_PARSE). */
+typedef struct gs_sdf_design {
+  int64_t num_gates, num_nets, num_cells;
+  const char *gate_names;  const int64_t *gate_name_off;   /* [G+1] byte offsets */
+  const char *net_names;   const int64_t *net_name_off;    /* [N+1] */
+  const char *pin_names;   const int64_t *pin_name_off;    /* all cells' input pin names */
+  const int64_t *cell_pin_first;                           /* [C+1] into the pin names */
+  const char *cell_outputs; const int64_t *cell_output_off; /* [C+1] */
+  const int64_t *gate_cell;                                /* [G] */
+  const int64_t *pin_off;                                  /* [G+1] */
+  const int64_t *pin_net;                                  /* [sum k] */
+  const int64_t *out_net;                                  /* [G] */
+} gs_sdf_design;
+typedef struct gs_sdf gs_sdf;
+int gs_sdf_parse(const char *text, int64_t len, const gs_sdf_design *design, int corner,
+                 const char *path, gs_sdf **out);
+/* sizes: condition rows R, pins, the document's timescale (fs), warnings */
+int gs_sdf_sizes(const gs_sdf *h, int64_t *num_rows, int64_t *num_pins, int64_t *timescale_fs,
+                 int64_t *num_warnings);
+int gs_sdf_copy(const gs_sdf *h, int64_t *arc_rows, int64_t *pin_ic);
+const char *gs_sdf_warning(const gs_sdf *h, int64_t i);
+int gs_sdf_destroy(gs_sdf *h);
+/* 1-based column of the last GS_ERR_PARSE (0 if none) */
+int64_t gs_last_error_col(void);
+
 /* ---- activity report writer (host): the format immediately downstream of
  * the path ------------------------------------------------ */
 

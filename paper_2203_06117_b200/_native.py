@@ -50,6 +50,17 @@ class ArenaOut(C.Structure):
                 ("offsets", _i64p), ("buf", _i64p), ("n_buf", C.c_int64)]
 
 
+class SdfDesign(C.Structure):
+    _fields_ = [("num_gates", C.c_int64), ("num_nets", C.c_int64), ("num_cells", C.c_int64),
+                ("gate_names", C.c_char_p), ("gate_name_off", _i64p),
+                ("net_names", C.c_char_p), ("net_name_off", _i64p),
+                ("pin_names", C.c_char_p), ("pin_name_off", _i64p),
+                ("cell_pin_first", _i64p),
+                ("cell_outputs", C.c_char_p), ("cell_output_off", _i64p),
+                ("gate_cell", _i64p), ("pin_off", _i64p), ("pin_net", _i64p),
+                ("out_net", _i64p)]
+
+
 class Timing(C.Structure):
     _fields_ = [("ms_total", C.c_float), ("ms_gate_eval", C.c_float), ("ms_stim", C.c_float),
                 ("launches", C.c_int64), ("gate_eval_launches", C.c_int64),
@@ -86,6 +97,13 @@ SIGNATURES = {
     "gs_vcd_copy": (C.c_int, [C.c_void_p, _i64p, _i64p, _u8p]),
     "gs_vcd_destroy": (C.c_int, [C.c_void_p]),
     "gs_last_error_line": (C.c_int64, []),
+    "gs_last_error_col": (C.c_int64, []),
+    "gs_sdf_parse": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(SdfDesign), C.c_int,
+                               C.c_char_p, C.POINTER(C.c_void_p)]),
+    "gs_sdf_sizes": (C.c_int, [C.c_void_p, _i64p, _i64p, _i64p, _i64p]),
+    "gs_sdf_copy": (C.c_int, [C.c_void_p, _i64p, _i64p]),
+    "gs_sdf_warning": (C.c_char_p, [C.c_void_p, C.c_int64]),
+    "gs_sdf_destroy": (C.c_int, [C.c_void_p]),
     "gs_saif_format": (C.c_int, [C.c_char_p, _i64p, C.c_int64, _i64p, _i64p, _i64p, _i64p,
                                  C.c_int64, C.c_char_p, C.c_char_p, C.c_int, C.c_char_p,
                                  C.c_int64, _i64p]),
@@ -165,6 +183,104 @@ def vcd_parse(text, pi_names, path=None):
     finally:
         lib.gs_vcd_destroy(h)
     return pi_off, pi_times, pi_init, int(dur.value)
+
+
+def _blob(strings):
+    """ASCII/UTF-8 strings -> (bytes, int64 byte offsets [n+1])."""
+    strings = list(strings)
+    joined = "".join(strings)
+    if joined.isascii():
+        lens = np.fromiter(map(len, strings), dtype=np.int64, count=len(strings))
+        blob = joined.encode("ascii")
+    else:
+        enc = [x.encode("utf-8", errors="surrogatepass") for x in strings]
+        lens = np.fromiter(map(len, enc), dtype=np.int64, count=len(enc))
+        blob = b"".join(enc)
+    off = np.zeros(len(strings) + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    return blob, off
+
+
+def _sdf_context(netlist):
+    """Flat netlist description for gs_sdf_parse, cached on the netlist."""
+    ctx = getattr(netlist, "_gs_sdf_ctx", None)
+    if ctx is not None:
+        return ctx
+    gates = netlist.gates
+    cells, cell_ix = [], {}
+    gate_cell = np.empty(len(gates), dtype=np.int64)
+    for i, g in enumerate(gates):
+        c = cell_ix.get(id(g.cell))
+        if c is None:
+            c = cell_ix[id(g.cell)] = len(cells)
+            cells.append(g.cell)
+        gate_cell[i] = c
+    k = np.fromiter((len(g.pin_nets) for g in gates), dtype=np.int64, count=len(gates))
+    pin_off = np.zeros(len(gates) + 1, dtype=np.int64)
+    np.cumsum(k, out=pin_off[1:])
+    pin_net = np.fromiter((n for g in gates for n in g.pin_nets), dtype=np.int64,
+                          count=int(pin_off[-1]))
+    out_net = np.fromiter((g.out_net for g in gates), dtype=np.int64, count=len(gates))
+    pins = [p for c in cells for p in c.input_pins]
+    first = np.zeros(len(cells) + 1, dtype=np.int64)
+    np.cumsum([len(c.input_pins) for c in cells], out=first[1:])
+    keep = {"gn": _blob(g.name for g in gates), "nn": _blob(netlist.net_names),
+            "pn": _blob(pins), "co": _blob(c.output_pin for c in cells),
+            "first": first, "gate_cell": gate_cell, "pin_off": pin_off, "pin_net": pin_net,
+            "out_net": out_net}
+    d = SdfDesign(num_gates=len(gates), num_nets=len(netlist.net_names), num_cells=len(cells))
+    d.gate_names, d.gate_name_off = keep["gn"][0], _p64(keep["gn"][1])
+    d.net_names, d.net_name_off = keep["nn"][0], _p64(keep["nn"][1])
+    d.pin_names, d.pin_name_off = keep["pn"][0], _p64(keep["pn"][1])
+    d.cell_pin_first = _p64(first)
+    d.cell_outputs, d.cell_output_off = keep["co"][0], _p64(keep["co"][1])
+    d.gate_cell, d.pin_off = _p64(gate_cell), _p64(pin_off)
+    d.pin_net, d.out_net = _p64(pin_net), _p64(out_net)
+    ctx = (d, keep)
+    try:
+        netlist._gs_sdf_ctx = ctx
+    except AttributeError:
+        pass
+    return ctx
+
+
+def sdf_parse(text, netlist, corner, path):
+    """Native SDF reader (``gs_sdf_parse``): -> ``(arc_rows [R, 2], pin_ic,
+    timescale_fs, warnings)`` or None (library not built / text outside the
+    native subset).  Raises the reference's ParseError / SemanticError."""
+    from .errors import ParseError, SemanticError
+    try:
+        lib = load()
+    except RuntimeError:
+        return None
+    try:
+        raw = text.encode("ascii") if isinstance(text, str) else bytes(text)
+    except UnicodeEncodeError:
+        return None
+    d, keep = _sdf_context(netlist)
+    h = C.c_void_p()
+    rc = lib.gs_sdf_parse(raw, len(raw), C.byref(d), ("min", "typ", "max").index(corner),
+                          str(path).encode("utf-8", errors="surrogatepass"), C.byref(h))
+    if rc == GS_ERR_UNSUPPORTED:
+        return None
+    if rc in (GS_ERR_PARSE, GS_ERR_SEMANTIC):
+        msg = (lib.gs_last_error() or b"").decode("utf-8", errors="surrogatepass")
+        if rc == GS_ERR_PARSE:
+            line, col = int(lib.gs_last_error_line()), int(lib.gs_last_error_col())
+            raise ParseError(msg, path, line or None, col or None)
+        raise SemanticError(msg)
+    _check(rc)
+    try:
+        r, p, ts, nw = (C.c_int64() for _ in range(4))
+        _check(lib.gs_sdf_sizes(h, C.byref(r), C.byref(p), C.byref(ts), C.byref(nw)))
+        arc = np.empty((r.value, 2), dtype=np.int64)
+        ic = np.empty(p.value, dtype=np.int64)
+        _check(lib.gs_sdf_copy(h, _p64(arc), _p64(ic)))
+        warns = [lib.gs_sdf_warning(h, i).decode("utf-8", errors="surrogatepass")
+                 for i in range(nw.value)]
+    finally:
+        lib.gs_sdf_destroy(h)
+    return arc, ic, int(ts.value), warns
 
 
 def saif_format(net_names, t0, t1, tc, ig, duration, design_name, version, include_ig):

@@ -14,17 +14,18 @@
 #include "glsim_cuda.h"
 #include "kernels.cuh"
 #include "vcd_reader.h"
+#include "sdf_reader.h"
 
 using namespace gs;
 
 namespace {
 
 thread_local std::string g_err;
-thread_local int64_t g_err_line = 0;
+thread_local int64_t g_err_line = 0, g_err_col = 0;
 
 int fail(int code, const std::string &msg) {
   g_err = msg;
-  g_err_line = 0;
+  g_err_line = g_err_col = 0;
   return code;
 }
 
@@ -843,6 +844,8 @@ const char *gs_last_error(void) { return g_err.c_str(); }
 
 int64_t gs_last_error_line(void) { return g_err_line; }
 
+int64_t gs_last_error_col(void) { return g_err_col; }
+
 int gs_device_count(int *count) {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
@@ -1165,6 +1168,101 @@ int gs_vcd_copy(const gs_vcd *v, int64_t *pi_off, int64_t *pi_times, uint8_t *pi
 
 int gs_vcd_destroy(gs_vcd *v) {
   delete v;
+  return GS_OK;
+}
+
+// ---- SDF reader
+
+}  // extern "C"
+
+struct gs_sdf {
+  gssdf::Result r;
+};
+
+extern "C" {
+
+int gs_sdf_parse(const char *text, int64_t len, const gs_sdf_design *dd, int corner,
+                 const char *path, gs_sdf **out) {
+  if (!out || !dd || (len > 0 && !text) || corner < 0 || corner > 2)
+    return fail(GS_ERR_ARG, "bad SDF reader argument");
+  *out = nullptr;
+  const int64_t G = dd->num_gates, Nn = dd->num_nets, Cn = dd->num_cells;
+  if (G < 0 || Nn < 0 || Cn < 0 || G > INT32_MAX || Nn > INT32_MAX)
+    return fail(GS_ERR_ARG, "design size out of range");
+  gssdf::Design d;
+  auto names = [](const char *blob, const int64_t *off, int64_t n, std::vector<std::string> &o) {
+    o.resize((size_t)n);
+    for (int64_t i = 0; i < n; ++i) o[i].assign(blob + off[i], (size_t)(off[i + 1] - off[i]));
+  };
+  names(dd->gate_names, dd->gate_name_off, G, d.gate_names);
+  names(dd->net_names, dd->net_name_off, Nn, d.net_names);
+  std::vector<std::string> pins;
+  const int64_t npins = Cn ? dd->cell_pin_first[Cn] : 0;
+  names(dd->pin_names, dd->pin_name_off, npins, pins);
+  names(dd->cell_outputs, dd->cell_output_off, Cn, d.cell_output);
+  d.cell_inputs.resize((size_t)Cn);
+  for (int64_t c = 0; c < Cn; ++c)
+    d.cell_inputs[c].assign(pins.begin() + dd->cell_pin_first[c],
+                            pins.begin() + dd->cell_pin_first[c + 1]);
+  d.gate_cell.resize((size_t)G);
+  d.pin_off.assign(dd->pin_off, dd->pin_off + G + 1);
+  d.out_net.assign(dd->out_net, dd->out_net + G);
+  for (int64_t g = 0; g < G; ++g) {
+    const int64_t c = dd->gate_cell[g];
+    if (c < 0 || c >= Cn) return fail(GS_ERR_ARG, "gate cell index out of range");
+    d.gate_cell[g] = (int)c;
+    const int64_t k = d.pin_off[g + 1] - d.pin_off[g];
+    if (k < 1 || k > 30 || k != (int64_t)d.cell_inputs[c].size())
+      return fail(GS_ERR_ARG, "gate fanin does not match its cell");
+    if (d.out_net[g] < 0 || d.out_net[g] >= Nn) return fail(GS_ERR_ARG, "out_net out of range");
+  }
+  const int64_t P = G ? d.pin_off[G] : 0;
+  d.pin_net.assign(dd->pin_net, dd->pin_net + P);
+  gs_sdf *h = new gs_sdf();
+  const gssdf::Status st = gssdf::parse(text, len, d, corner, path ? path : "<sdf>", h->r);
+  if (st != gssdf::SDF_OK) {
+    const std::string msg = h->r.msg;
+    const int64_t line = h->r.line, col = h->r.col;
+    delete h;
+    if (st == gssdf::SDF_FALLBACK)
+      return fail(GS_ERR_UNSUPPORTED, "SDF text outside the native reader's subset");
+    const int rc = fail(st == gssdf::SDF_PARSE ? GS_ERR_PARSE : GS_ERR_SEMANTIC, msg);
+    if (st == gssdf::SDF_PARSE) {
+      g_err_line = line;
+      g_err_col = col;
+    }
+    return rc;
+  }
+  *out = h;
+  return GS_OK;
+}
+
+int gs_sdf_sizes(const gs_sdf *h, int64_t *num_rows, int64_t *num_pins, int64_t *timescale_fs,
+                 int64_t *num_warnings) {
+  if (!h || !num_rows || !num_pins || !timescale_fs || !num_warnings)
+    return fail(GS_ERR_ARG, "null argument");
+  *num_rows = (int64_t)h->r.arc_rows.size() / 2;
+  *num_pins = (int64_t)h->r.pin_ic.size();
+  *timescale_fs = h->r.timescale_fs;
+  *num_warnings = (int64_t)h->r.warnings.size();
+  return GS_OK;
+}
+
+int gs_sdf_copy(const gs_sdf *h, int64_t *arc_rows, int64_t *pin_ic) {
+  if (!h || (!arc_rows && !h->r.arc_rows.empty()) || (!pin_ic && !h->r.pin_ic.empty()))
+    return fail(GS_ERR_ARG, "null argument");
+  std::copy(h->r.arc_rows.begin(), h->r.arc_rows.end(), arc_rows);
+  std::copy(h->r.pin_ic.begin(), h->r.pin_ic.end(), pin_ic);
+  return GS_OK;
+}
+
+const char *gs_sdf_warning(const gs_sdf *h, int64_t i) {
+  if (!h || i < 0 || i >= (int64_t)h->r.warnings.size()) return nullptr;
+  return h->r.warnings[(size_t)i].c_str();
+}
+
+int gs_sdf_destroy(gs_sdf *h) {
+  delete h;
   return GS_OK;
 }
 
