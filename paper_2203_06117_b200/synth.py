@@ -209,12 +209,23 @@ def stimulus(cfg, w_lo=0, w_hi=None, rebase=True):
     return StimulusSet.from_csr(b, pi_off, times, init)
 
 
-def _parity_before(cfg, w_lo, block=4096):
-    par = np.zeros(cfg.num_inputs, dtype=np.uint8)
+def _parity_before(cfg, w_lo, block=2048):
+    """Per input, parity of its toggle count over windows [0, w_lo): only the
+    toggle decision of stimulus_arrays (u < alpha, as the integer test
+    h1 >> 11 < ceil(alpha * 2^53)) is evaluated."""
+    P = cfg.num_inputs
+    par = np.zeros(P, dtype=np.uint64)
+    p = np.arange(P, dtype=np.uint64)[:, None]
+    is_ppi = (np.arange(P) < cfg.ppis)[:, None]
+    alpha = np.where(is_ppi, cfg.ppi_alpha, cfg.pi_alpha)
+    thr = np.ceil(alpha * float(1 << 53)).astype(np.uint64)
+    base = (np.uint64(cfg.seed) << np.uint64(56)) ^ (p << np.uint64(32))
     for a in range(0, w_lo, block):
-        off, _, _ = stimulus_arrays(cfg, a, min(w_lo, a + block))
-        par ^= (np.diff(off) & 1).astype(np.uint8)
-    return par
+        w = np.arange(a, min(w_lo, a + block), dtype=np.uint64)[None, :]
+        with np.errstate(over="ignore"):
+            h1 = _splitmix64(base ^ w)
+        par ^= ((h1 >> np.uint64(11)) < thr).sum(axis=1, dtype=np.uint64) & np.uint64(1)
+    return par.astype(np.uint8)
 
 
 def work_units(cfg, windows):
