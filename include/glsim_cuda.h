@@ -164,6 +164,25 @@ int gs_last_timing(gs_engine *e, gs_timing *t);
 int gs_run_stats_device(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct,
                         int64_t *acc_dev);
 
+/* Device-side cross-check of a run against reference waveforms (SURVEY
+ * §8(f) item 4; the host compare_waveforms, pkg/src/glsim/oracle.py:201-226):
+ * simulates windows [w_lo, w_hi) and compares, on the GPU, every gate's
+ * window-start value, toggle count and toggle times with `ref` -- a reference
+ * arena in the layout of gs_arena_out ([G][cols] offsets / counts / initials,
+ * absolute int64 times in buf, column 0 = window w_lo).  Returns the number
+ * of mismatching (gate, window) pairs and the first one (gate, absolute
+ * window; -1 when none). */
+typedef struct gs_arena_ref {
+  const int64_t *buf;
+  int64_t n_buf;
+  const int64_t *offsets, *counts;
+  const uint8_t *initials;
+  int64_t cols;
+} gs_arena_ref;
+int gs_run_compare(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct,
+                   const gs_arena_ref *ref, int64_t *mismatches, int64_t *first_gate,
+                   int64_t *first_window);
+
 /* ---- kernel-seam entry points: same arguments as the reference's numba
  * kernels, host arrays in and out, executed on the GPU ------------------- */
 

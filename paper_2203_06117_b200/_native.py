@@ -61,6 +61,11 @@ class SdfDesign(C.Structure):
                 ("out_net", _i64p)]
 
 
+class ArenaRef(C.Structure):
+    _fields_ = [("buf", _i64p), ("n_buf", C.c_int64), ("offsets", _i64p), ("counts", _i64p),
+                ("initials", _u8p), ("cols", C.c_int64)]
+
+
 class Timing(C.Structure):
     _fields_ = [("ms_total", C.c_float), ("ms_gate_eval", C.c_float), ("ms_stim", C.c_float),
                 ("launches", C.c_int64), ("gate_eval_launches", C.c_int64),
@@ -86,6 +91,8 @@ SIGNATURES = {
     "gs_last_timing": (C.c_int, [C.c_void_p, C.POINTER(Timing)]),
     "gs_run_stats_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
                                       C.c_void_p]),
+    "gs_run_compare": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                                 C.POINTER(ArenaRef), _i64p, _i64p, _i64p]),
     "gs_dwell_sweep": (C.c_int, [C.c_int64, _u8p, _i64p, _i64p, C.c_int64, _i64p, _i64p, _u8p,
                                  C.c_int64, C.c_int64, _i64p, C.c_int64, _i64p, _i64p, _u8p,
                                  C.c_int64, C.c_int64, _i64p, C.c_int64, C.c_int64, C.c_int64,
@@ -432,6 +439,19 @@ class Engine:
         """Add stats of [w_lo, w_hi) into a device int64 buffer [3N+3] at acc_ptr."""
         _check(load().gs_run_stats_device(self.handle, stim.handle, int(w_lo), int(w_hi),
                                           int(pct), C.c_void_p(acc_ptr)))
+
+    def run_compare(self, stim, w_lo, w_hi, pct, buf, offsets, counts, initials):
+        """Simulate [w_lo, w_hi) and compare every gate waveform with a
+        reference arena on the device (``gs_run_compare``): -> (mismatching
+        (gate, window) pairs, first (gate, window) or None)."""
+        buf, offsets, counts = _c64(buf), _c64(offsets), _c64(counts)
+        initials = _c8(initials)
+        ref = ArenaRef(buf=_p64(buf), n_buf=buf.size, offsets=_p64(offsets),
+                       counts=_p64(counts), initials=_p8(initials), cols=offsets.shape[1])
+        n, g, w = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(load().gs_run_compare(self.handle, stim.handle, int(w_lo), int(w_hi), int(pct),
+                                     C.byref(ref), C.byref(n), C.byref(g), C.byref(w)))
+        return int(n.value), ((int(g.value), int(w.value)) if n.value else None)
 
     def run_arena(self, stim, w_lo, w_hi, pct, offsets=None, n_buf=0, want_stats=False):
         """Count pass (offsets None) or store pass over [w_lo, w_hi).

@@ -545,6 +545,7 @@ struct RunOut {
   gs_arena_out *arena;      // may be null
   int64_t w_base;           // first window of the arena's column range
   int64_t arena_cols;       // Ws (host row pitch)
+  CompareDev *cmp = nullptr;  // device cross-check against a reference arena (K7)
 };
 
 template <typename TS, int MODE>
@@ -750,7 +751,15 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     launches += k1 + nl;
     eval_launches += nl;
     ++chunks;
-    // ---- results of the chunk
+    // ---- results of the chunk (the chunk is complete here: no pool re-run)
+    if (ro.cmp && G > 0) {
+      CompareDev X = *ro.cmp;
+      X.col0 = w - ro.w_base;
+      const int64_t items = G * (int64_t)Tc;
+      const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, e->sms * 16));
+      compare_arena<TS><<<blocks, 256, 0, e->st>>>(Dd, C, X);
+      CK(cudaGetLastError());
+    }
     {
       const int threads = 256;
       const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((N + threads - 1) / threads, 4096));
@@ -958,6 +967,59 @@ int gs_run_stats(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, 
   RunOut ro{e->acc_run, nullptr, w_lo, w_hi - w_lo};
   TRY(run_mode<MODE_STATS>(e, s, w_lo, w_hi, pct, ro));
   return finish_stats(e, out);
+}
+
+int gs_run_compare(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct,
+                   const gs_arena_ref *ref, int64_t *mismatches, int64_t *first_gate,
+                   int64_t *first_window) {
+  TRY(check_run(e, s, w_lo, w_hi, pct));
+  if (!ref || !mismatches || !first_gate || !first_window)
+    return fail(GS_ERR_ARG, "null compare argument");
+  const int64_t G = e->d->G, Ws = w_hi - w_lo;
+  if (ref->cols < Ws || (G * Ws > 0 && (!ref->offsets || !ref->counts || !ref->initials)))
+    return fail(GS_ERR_ARG, "reference arena does not cover the window range");
+  for (int64_t g = 0; g < G; ++g)
+    for (int64_t w = 0; w < Ws; ++w) {
+      const int64_t o = ref->offsets[g * ref->cols + w], c = ref->counts[g * ref->cols + w];
+      if (c < 0 || o < 0 || o + c > ref->n_buf) return fail(GS_ERR_ARG, "reference arena out of range");
+    }
+  long long *buf = nullptr, *off = nullptr, *cnt = nullptr;
+  unsigned char *ini = nullptr;
+  unsigned long long *bad = nullptr;
+  int rc = [&]() -> int {
+    TRY(upload(&buf, (const long long *)ref->buf, (size_t)ref->n_buf));
+    TRY(upload(&off, (const long long *)ref->offsets, (size_t)(G * ref->cols)));
+    TRY(upload(&cnt, (const long long *)ref->counts, (size_t)(G * ref->cols)));
+    TRY(upload(&ini, ref->initials, (size_t)(G * ref->cols)));
+    TRY(dalloc(&bad, 2));
+    const unsigned long long init[2] = {0ull, ~0ull};
+    CK(cudaMemcpy(bad, init, sizeof(init), cudaMemcpyHostToDevice));
+    CompareDev X;
+    X.buf = buf;
+    X.offsets = off;
+    X.counts = cnt;
+    X.initials = ini;
+    X.cols = ref->cols;
+    X.col0 = 0;
+    X.G = (int)G;
+    X.bad = bad;
+    CK(cudaMemsetAsync(e->acc_run, 0, sizeof(long long) * (3 * (size_t)e->d->N + 3), e->st));
+    RunOut ro{e->acc_run, nullptr, w_lo, Ws, &X};
+    TRY(run_mode<MODE_STATS>(e, s, w_lo, w_hi, pct, ro));
+    unsigned long long h[2];
+    CK(cudaStreamSynchronize(e->st));
+    CK(cudaMemcpy(h, bad, sizeof(h), cudaMemcpyDeviceToHost));
+    *mismatches = (int64_t)h[0];
+    *first_gate = h[0] ? (int64_t)(h[1] >> 32) : -1;
+    *first_window = h[0] ? (int64_t)(h[1] & 0xFFFFFFFFull) + w_lo : -1;
+    return GS_OK;
+  }();
+  dfree(buf);
+  dfree(off);
+  dfree(cnt);
+  dfree(ini);
+  dfree(bad);
+  return rc;
 }
 
 int gs_run_arena(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct,

@@ -1334,6 +1334,63 @@ __global__ void chunk_windows(ChunkDev C) {
     C.wlen32[w] = w < C.Wc ? (unsigned)(C.bnd[C.w0 + w + 1] - C.bnd[C.w0 + w]) : 0u;
 }
 
+// ------------------------------------------------------------------- K7
+// Device-side waveform cross-check (the host
+// compare_waveforms, reference oracle.py:201-226): every gate waveform of the
+// chunk -- start value, toggle count and each toggle time -- against reference
+// waveforms uploaded in the reference arena layout ([G][cols] offsets / counts
+// / initials into an absolute-time buffer).  Warp per (gate, 128-window tile),
+// lane = 4 windows.  Counts mismatching (gate, window) pairs and keeps the
+// first one in (gate, window) order.
+struct CompareDev {
+  const long long *buf, *offsets, *counts;
+  const unsigned char *initials;
+  long long cols;          // reference row pitch
+  long long col0;          // reference column of the chunk's first window
+  int G;
+  unsigned long long *bad;  // [0] mismatching pairs, [1] first (gate << 32 | window), ~0 none
+};
+
+template <typename TS>
+__global__ void compare_arena(DesignDev D, ChunkDev C, CompareDev X) {
+  const unsigned lane = lane_id();
+  const long long warps = (long long)gridDim.x * (blockDim.x / kWarp);
+  const long long items = (long long)X.G * C.Tc;
+  const TS *data = reinterpret_cast<const TS *>(C.data);
+  const int Tw = C.Wpad / 32;
+  for (long long it = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
+       it < items; it += warps) {
+    const int g = (int)(it / C.Tc), t = (int)(it % C.Tc);
+    const int net = D.P + g;
+    const int wl = t * kTile + (int)lane * kWPL;
+    unsigned c[kWPL], s = 0;
+    load_counts(C.cnt + (size_t)net * C.Wpad + wl, c);
+#pragma unroll
+    for (int j = 0; j < kWPL; ++j) s += c[j];
+    unsigned tot;
+    unsigned pos = warp_excl_scan(s, &tot);
+    const unsigned long long tb = __ldg(C.tbase + (size_t)net * C.Tc + t);
+    const unsigned bits = load_init_bits(C.init + (size_t)net * Tw, t);
+#pragma unroll
+    for (int j = 0; j < kWPL; ++j) {
+      const int w = wl + j;
+      if (w >= C.Wc) break;
+      const long long col = X.col0 + w;
+      const size_t r = (size_t)g * X.cols + col;
+      const long long rc = X.counts[r], ro = X.offsets[r];
+      bool ok = ((bits >> j) & 1u) == (unsigned)(X.initials[r] & 1u) && rc == (long long)c[j];
+      const long long b_lo = C.bnd[C.w0 + w];
+      for (unsigned q = 0; ok && q < c[j]; ++q)
+        ok = (long long)data[tb + pos + q] + b_lo == X.buf[ro + q];
+      if (!ok) {
+        atomicAdd(X.bad, 1ull);
+        atomicMin(X.bad + 1, ((unsigned long long)g << 32) | (unsigned long long)col);
+      }
+      pos += c[j];
+    }
+  }
+}
+
 // chunk accumulators -> run accumulators [t1 | tc | ig | filtered, icf, disc]
 __global__ void acc_commit(const long long *__restrict__ acc, long long *__restrict__ out, int N) {
   __shared__ unsigned long long part[3];

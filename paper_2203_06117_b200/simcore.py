@@ -297,6 +297,22 @@ class _Session:
         return s
 
 
+def compare_on_device(model, stimuli, reference, window_range=None, pathpulse_pct=100):
+    """Simulate ``window_range`` on the GPU and check every gate waveform
+    against ``reference`` -- an arena in the reference layout (``buf``,
+    ``offsets``, ``counts``, ``initials`` as attributes or keys, [G, Ws],
+    absolute times; e.g. the oracle's) -- on the device (``gs_run_compare``,
+    SURVEY §8(f) item 4), without copying the engine's waveforms back.
+    Returns ``(mismatching (gate, window) pairs, first (gate, window) or None)``.
+    """
+    def get(k):
+        return reference[k] if isinstance(reference, dict) else getattr(reference, k)
+    w_lo, w_hi = window_range if window_range is not None else (0, stimuli.num_windows)
+    s = _Session.get(model, stimuli)
+    return s.engine.run_compare(s.stim, w_lo, w_hi, pathpulse_pct, get("buf"), get("offsets"),
+                                get("counts"), get("initials"))
+
+
 def _trace(model, task_trace, task_counts, w_lo):
     # one entry per level launch, in level order: the level barrier is the
     # kernel boundary (what the reference's task_trace ramps assert)

@@ -46,3 +46,22 @@ def test_full_size_design_on_sampled_windows(oracle_lib, name, ranges):
         assert diag["discarded"] == int(a["discarded"].sum())
         assert diag["ic_filtered"] == int(a["ic_filtered"].sum())
         assert int(stats.tc.sum()) > 0
+
+
+@pytest.mark.parametrize("name,lo,hi", [("C3", 2, 5), ("C4", 11, 12)])
+def test_full_size_waveforms_on_device(oracle_lib, name, lo, hi):
+    # every gate waveform of the full-size design (1M / 10M gates) on sampled
+    # windows, checked on the device against the oracle's arena (K7) -- and a
+    # perturbed reference is caught at the perturbed (gate, window)
+    cfg = synth.config(name)
+    m = synth.design(cfg)
+    stim = synth.stimulus(cfg, lo, hi)
+    _, a = _oracle_stats(oracle_lib, m, stim, cfg.pct)
+    bad, first = api.compare_on_device(m, stim, a, pathpulse_pct=cfg.pct)
+    assert (bad, first) == (0, None)
+    counts = a["counts"]
+    g, w = map(int, np.argwhere(counts > 0)[len(np.argwhere(counts > 0)) // 2])
+    buf = a["buf"].copy()
+    buf[a["offsets"][g, w]] += 1
+    bad, first = api.compare_on_device(m, stim, dict(a, buf=buf), pathpulse_pct=cfg.pct)
+    assert (bad, first) == (1, (g, w))
