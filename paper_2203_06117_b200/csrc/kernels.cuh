@@ -70,11 +70,11 @@ constexpr int kWPL = kTile / kWarp;         // windows per lane in the cooperati
 constexpr int kEvalWarps = 4;               // warps per K4 CTA
 constexpr int kEvalThreads = kEvalWarps * kWarp;
 // staged words per warp (smem): as large as each fixed-k kernel's occupancy
-// allows (6 CTAs of 4 warps for k <= 2, 5 for k = 3, 4), so that few tiles
-// overflow to the in-place path
+// allows (7 CTAs of 4 warps for k = 1, 6 for k = 2, 5 for k = 3, 4), so that
+// few tiles overflow to the in-place path
 template <int KM>
 __host__ __device__ constexpr int slab_words() {
-  return KM == 1 || KM == 2 ? 1280 : KM == 3 ? 1536 : KM == 4 ? 1152 : 1024;
+  return KM == 1 ? 1000 : KM == 2 ? 1280 : KM == 3 ? 1536 : KM == 4 ? 1152 : 1024;
 }
 constexpr int kMaxK = 16;                   // netlist.py:17 MAX_CELL_INPUTS
 constexpr long long kInf = LLONG_MAX;
@@ -1253,7 +1253,7 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
 // the next item (gate, group of tpi tiles) from a per-launch counter and owns
 // a private output region (no CTA barrier, no global atomics on the data path).
 template <typename TS, typename TT, int MODE, int K, bool PCT100>
-__global__ void __launch_bounds__(kEvalThreads, (K == 0 ? 4 : K >= 3 ? 5 : 6))
+__global__ void __launch_bounds__(kEvalThreads, (K == 0 ? 4 : K >= 3 ? 5 : K == 1 ? 7 : 6))
 gate_eval(DesignDev D, ChunkDev C, LevelArgs A) {
   constexpr int KM = K > 0 ? K : kMaxK;
   using SM = TileSmem<TS, TT, KM>;
