@@ -291,18 +291,19 @@ def test_c_abi_rejects_malformed_stimulus_on_device():
 SLAB = {1: 1280, 2: 1280, 3: 1536, 4: 1152}
 
 
-@pytest.mark.parametrize("seed,max_toggles", [(1, 250), (2, 700), (3, 1500), (4, 4000)])
-def test_busy_tiles_take_every_staging_path(oracle_lib, seed, max_toggles):
+@pytest.mark.parametrize("seed,max_toggles,pct", [(1, 250, 100), (2, 700, 100), (3, 1500, 100),
+                                                  (4, 4000, 100), (2, 700, 50), (3, 1500, 0)])
+def test_busy_tiles_take_every_staging_path(oracle_lib, seed, max_toggles, pct):
     # Tiles with many fanin toggles leave the fully staged fast path: inputs in
     # shared memory with outputs staged in the pool (UB <= slab < 2 UB), or both
     # read and staged in global memory (UB > slab).  All must agree with the
     # oracle; the instances are checked to actually reach those paths.
     docs = gen.make_docs(9100 + seed, n_gates=240, n_pis=6, windows=6, duration_ps=60_000,
-                         max_toggles=max_toggles, max_delay=1_500, max_levels=5)
+                         max_toggles=max_toggles, max_delay=1_500, max_levels=5, pct=pct)
     nl, lv, delays, stim, arena, diag, stats = gpu_run(docs)
     waves = gen.load(docs, api)[3]
     d, st, oa, os_ = oracle_lib.simulate(lv, delays, gen.oracle_inputs(nl, waves),
-                                         stim.boundaries, threads=4)
+                                         stim.boundaries, pct=pct, threads=4)
     for f in ("buf", "offsets", "caps", "counts", "initials", "filtered", "ic_filtered",
               "discarded"):
         assert np.array_equal(getattr(arena, f), oa[f]), f"arena.{f}"
