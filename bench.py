@@ -307,8 +307,9 @@ def main():
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            if pj.get("config") == cfg.name and pj.get("windows") == Wr:
-                traffic = pj.get("dram_bytes_per_launch")
+            for ent in (pj if isinstance(pj, list) else [pj]):
+                if ent.get("config") == cfg.name and ent.get("windows") == Wr:
+                    traffic = ent.get("dram_bytes_per_launch")
         except Exception:
             pass
 
