@@ -49,7 +49,16 @@ template <typename T>
 int dalloc(T **p, size_t n) {
   *p = nullptr;
   if (n == 0) n = 1;
-  CK(cudaMalloc((void **)p, n * sizeof(T)));
+  const cudaError_t e = cudaMalloc((void **)p, n * sizeof(T));
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    return fail(e == cudaErrorMemoryAllocation ? GS_ERR_CAPACITY : GS_ERR_CUDA,
+                std::string(cudaGetErrorString(e)) + " allocating " +
+                    std::to_string(n * sizeof(T)) + " bytes (" + std::to_string(fr) +
+                    " of " + std::to_string(tot) + " free)");
+  }
   return GS_OK;
 }
 
@@ -780,10 +789,13 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
                              cudaMemcpyDeviceToHost, e->st));
       CK(cudaStreamSynchronize(e->st));
     }
-    // adapt: aim the next chunk at ~60% of the measured per-CTA region fill
+    // adapt: a pool well under-filled lets the next chunk grow, but never
+    // past the metadata share of the budget the first chunk was sized by
     if (used_words > 0) {
       const double fill = (double)used_words / (double)pool_words;
-      if (fill < 0.3 && wc == Wc) Wc = std::min<int64_t>(round_up(total, kTile), Wc * 2);
+      const int64_t meta_cap = std::max<int64_t>(kTile, (e->budget * 2 / 5) / per_win / kTile * kTile);
+      if (fill < 0.3 && wc == Wc)
+        Wc = std::min<int64_t>({round_up(total, kTile), Wc * 2, std::max<int64_t>(Wc, meta_cap)});
     }
     w += wc;
   }
