@@ -38,7 +38,7 @@ def parse_args():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--windows", type=int, default=0, help="windows per GPU (0 = config's)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-windows", type=int, default=0,
                     help="CPU baseline sample windows (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -261,23 +261,50 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        e2e_steps = []
-        for _ in range(args.e2e_steps):
-            x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            x0.record(stream)
+        # serial breakdown of one step (second of two: the stimulus pool is
+        # warm): upload, then simulate and read back
+        for _ in range(2):
             h0 = time.perf_counter()
             s2 = _native.Stimulus(dev, hstim)          # H2D of this step's stimulus
             h1 = time.perf_counter()
             step(s2)
             host_acc.copy_(acc, non_blocking=True)     # D2H of the per-net sums
-            x1.record(stream)
             stream.synchronize()
             h2 = time.perf_counter()
             del s2
-            e2e_steps.append((x0.elapsed_time(x1), 1e3 * (h1 - h0), 1e3 * (h2 - h1)))
-        e2e_ms = statistics.median(x[0] for x in e2e_steps)
-        e2e_upload_ms = statistics.median(x[1] for x in e2e_steps)
-        e2e_run_ms = statistics.median(x[2] for x in e2e_steps)
+        e2e_upload_ms, e2e_run_ms = 1e3 * (h1 - h0), 1e3 * (h2 - h1)
+        # end to end, as a streaming user runs it: step i+1's stimulus upload
+        # (gs_stim_create: pinned H2D + device validation, on its own stream
+        # from a worker thread) overlaps step i's simulation; every step still
+        # uploads its inputs and reads its sums back inside the timed region
+        from concurrent.futures import ThreadPoolExecutor
+        K = max(1, args.e2e_steps)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with ThreadPoolExecutor(1) as ex:
+            # untimed: one overlapped step, so the stimulus pool holds two
+            # stimuli (its growth is a one-off, not a per-step cost)
+            fut = ex.submit(_native.Stimulus, dev, hstim)
+            s_w = _native.Stimulus(dev, hstim)
+            step(s_w)
+            stream.synchronize()
+            del s_w
+            fut.result()
+            del fut
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fut = ex.submit(_native.Stimulus, dev, hstim)
+            for i in range(K):
+                s_i = fut.result()
+                if i + 1 < K:
+                    fut = ex.submit(_native.Stimulus, dev, hstim)
+                step(s_i)
+                host_acc.copy_(acc, non_blocking=True)
+                stream.synchronize()
+                del s_i
+            t1 = time.perf_counter()
+        e2e_ms = 1e3 * (t1 - t0) / K
 
     # max over ranks
     tm = torch.tensor([ms, e2e_ms, eval_ms], dtype=torch.float64, device="cuda")
@@ -339,7 +366,9 @@ def main():
                              "bytes_per_gate_window": bytes_step / (cfg.gates * Wr)},
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                        "steps": args.e2e_steps, "stat": "median per-step",
+                        "steps": K, "stat": "wall clock over the steps / steps (step i+1's "
+                        "upload overlapped with step i)", "serial_ms_per_step":
+                        e2e_upload_ms + e2e_run_ms,
                         "host_ms_stim_upload": e2e_upload_ms, "host_ms_run": e2e_run_ms},
                 "clocks": clocks, "gpu_launches": launches,
                 "activity": {"input_toggles_per_gw": in_tog / (cfg.gates * Wr),

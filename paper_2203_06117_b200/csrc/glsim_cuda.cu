@@ -89,32 +89,45 @@ int pool_ready(int dev) {
   return GS_OK;
 }
 
-template <typename T>
-int upload_pooled(T **p, const T *src, size_t n) {
-  *p = nullptr;
-  CK(cudaMallocAsync((void **)p, (n ? n : 1) * sizeof(T), (cudaStream_t)0));
-  if (n) CK(cudaMemcpy(*p, src, n * sizeof(T), cudaMemcpyHostToDevice));
+// The stimulus is uploaded, validated and freed on a per-device stream of
+// its own (non-blocking), so a stimulus for the next step can be created from
+// another host thread while an engine simulates the current one.
+int upload_stream(int dev, cudaStream_t *us) {
+  static cudaStream_t streams[64] = {};
+  if (dev < 0 || dev >= 64) return fail(GS_ERR_ARG, "device index out of range");
+  if (!streams[dev]) CK(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+  *us = streams[dev];
   return GS_OK;
 }
 
 template <typename T>
-void dfree_pooled(T *&p) {
-  if (p) cudaFreeAsync((void *)p, (cudaStream_t)0);
+int upload_pooled(T **p, const T *src, size_t n, cudaStream_t us) {
+  *p = nullptr;
+  CK(cudaMallocAsync((void **)p, (n ? n : 1) * sizeof(T), us));
+  if (n) CK(cudaMemcpyAsync(*p, src, n * sizeof(T), cudaMemcpyHostToDevice, us));
+  return GS_OK;
+}
+
+template <typename T>
+void dfree_pooled(T *&p, cudaStream_t us) {
+  if (p) cudaFreeAsync((void *)p, us);
   p = nullptr;
 }
 
 // run a validation kernel that ORs flags into a device int; return the flags
+// (synchronises the upload stream: the stimulus is complete on return)
 template <typename F>
-int device_check(int *flags, F launch) {
+int device_check(int *flags, cudaStream_t us, F launch) {
   int *f = nullptr;
-  TRY(dalloc(&f, 1));
-  cudaError_t e = cudaMemset(f, 0, sizeof(int));
+  CK(cudaMallocAsync((void **)&f, sizeof(int), us));
+  cudaError_t e = cudaMemsetAsync(f, 0, sizeof(int), us);
   if (e == cudaSuccess) {
     launch(f);
     e = cudaGetLastError();
   }
-  if (e == cudaSuccess) e = cudaMemcpy(flags, f, sizeof(int), cudaMemcpyDeviceToHost);
-  cudaFree(f);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(flags, f, sizeof(int), cudaMemcpyDeviceToHost, us);
+  cudaFreeAsync(f, us);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(us);
   if (e != cudaSuccess) return fail(GS_ERR_CUDA, cudaGetErrorString(e));
   return GS_OK;
 }
@@ -325,11 +338,14 @@ struct gs_stim {
     S.initials = initials;
     return S;
   }
+  cudaStream_t us = nullptr;  // upload stream of the device
   void release() {
-    // engine streams may still read the stimulus: drain the device first
-    cudaDeviceSynchronize();
-    dfree_pooled(bnd); dfree_pooled(pi_off); dfree_pooled(pi_times); dfree_pooled(buf);
-    dfree_pooled(offsets); dfree_pooled(counts); dfree_pooled(pi_init); dfree_pooled(initials);
+    // engine runs are synchronous: no engine work reads the stimulus once a
+    // run call has returned, so the buffers go back to the pool in order
+    // behind the upload stream's own work
+    dfree_pooled(bnd, us); dfree_pooled(pi_off, us); dfree_pooled(pi_times, us);
+    dfree_pooled(buf, us); dfree_pooled(offsets, us); dfree_pooled(counts, us);
+    dfree_pooled(pi_init, us); dfree_pooled(initials, us);
   }
 };
 
@@ -352,7 +368,9 @@ static int stim_build(gs_design *D, const gs_stim_desc *s, gs_stim *S) {
   S->csr = s->pi_off != nullptr;
   TRY(use_device(D->device));
   TRY(pool_ready(D->device));
-  TRY(upload_pooled(&S->bnd, (const long long *)s->boundaries, S->W + 1));
+  TRY(upload_stream(D->device, &S->us));
+  cudaStream_t us = S->us;
+  TRY(upload_pooled(&S->bnd, (const long long *)s->boundaries, S->W + 1, us));
   const int64_t P = S->P, W = S->W;
   if (S->csr) {
     if (!s->pi_times || !s->pi_init) return fail(GS_ERR_ARG, "incomplete CSR stimulus");
@@ -360,12 +378,12 @@ static int stim_build(gs_design *D, const gs_stim_desc *s, gs_stim *S) {
     for (int64_t p = 0; p < P; ++p)
       if (s->pi_off[p + 1] < s->pi_off[p]) return fail(GS_ERR_ARG, "pi_off not monotone");
     S->n_toggles = s->pi_off[P];
-    TRY(upload_pooled(&S->pi_off, (const long long *)s->pi_off, P + 1));
-    TRY(upload_pooled(&S->pi_times, (const long long *)s->pi_times, S->n_toggles));
-    TRY(upload_pooled(&S->pi_init, s->pi_init, P));
+    TRY(upload_pooled(&S->pi_off, (const long long *)s->pi_off, P + 1, us));
+    TRY(upload_pooled(&S->pi_times, (const long long *)s->pi_times, S->n_toggles, us));
+    TRY(upload_pooled(&S->pi_init, s->pi_init, P, us));
     int bad = 0;
-    TRY(device_check(&bad, [&](int *flag) {
-      stim_check_csr<<<std::max<int64_t>(1, std::min<int64_t>((P + 7) / 8, 4096)), 256>>>(
+    TRY(device_check(&bad, us, [&](int *flag) {
+      stim_check_csr<<<std::max<int64_t>(1, std::min<int64_t>((P + 7) / 8, 4096)), 256, 0, us>>>(
           S->pi_off, S->pi_times, (int)P, flag);
     }));
     if (bad) return fail(GS_ERR_ARG, "input toggle times must be strictly increasing");
@@ -373,14 +391,15 @@ static int stim_build(gs_design *D, const gs_stim_desc *s, gs_stim *S) {
     if (!s->buf && s->n_buf) return fail(GS_ERR_ARG, "missing stimulus buffer");
     if (!s->offsets || !s->counts || !s->initials) return fail(GS_ERR_ARG, "incomplete windowed stimulus");
     S->n_toggles = s->n_buf;
-    TRY(upload_pooled(&S->buf, (const long long *)s->buf, s->n_buf));
-    TRY(upload_pooled(&S->offsets, (const long long *)s->offsets, P * W));
-    TRY(upload_pooled(&S->counts, (const long long *)s->counts, P * W));
-    TRY(upload_pooled(&S->initials, s->initials, P * W));
+    TRY(upload_pooled(&S->buf, (const long long *)s->buf, s->n_buf, us));
+    TRY(upload_pooled(&S->offsets, (const long long *)s->offsets, P * W, us));
+    TRY(upload_pooled(&S->counts, (const long long *)s->counts, P * W, us));
+    TRY(upload_pooled(&S->initials, s->initials, P * W, us));
     int bad = 0;
-    TRY(device_check(&bad, [&](int *flag) {
+    TRY(device_check(&bad, us, [&](int *flag) {
       stim_check_win<<<(int)std::max<int64_t>(1, std::min<int64_t>((P * W + 255) / 256, 4096)),
-                       256>>>(S->buf, s->n_buf, S->offsets, S->counts, S->bnd, W, P * W, flag);
+                       256, 0, us>>>(S->buf, s->n_buf, S->offsets, S->counts, S->bnd, W, P * W,
+                                     flag);
     }));
     if (bad & BAD_REGION) return fail(GS_ERR_ARG, "stimulus window region out of range");
     if (bad) return fail(GS_ERR_ARG, "stimulus toggle outside its window or not increasing");
