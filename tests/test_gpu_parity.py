@@ -318,3 +318,28 @@ def test_busy_tiles_take_every_staging_path(oracle_lib, seed, max_toggles, pct):
     hybrid = int(((ub <= slab) & (2 * ub > slab)).sum())
     glob = int((ub > slab).sum())
     assert hybrid + glob > 0, "instance never leaves the fully staged path"
+
+
+def test_stimulus_upload_overlaps_a_running_simulation():
+    # gs_stim_create runs on its own stream: a stimulus created from a worker
+    # thread while the engine simulates (the overlapped e2e pattern) must give
+    # the same per-net sums as the serial sequence
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2203_06117_b200 import _native, synth
+    cfg = synth.config("C2", gates=20_000, windows=512)
+    m = synth.design(cfg)
+    stim = synth.stimulus(cfg, 0, 512)
+    dev = m.device()
+    eng = _native.Engine(dev, 0)
+    ref = eng.run_stats(_native.Stimulus(dev, stim), 0, 512, cfg.pct)
+    with ThreadPoolExecutor(1) as ex:
+        fut = ex.submit(_native.Stimulus, dev, stim)
+        for _ in range(4):
+            s = fut.result()
+            fut = ex.submit(_native.Stimulus, dev, stim)
+            got = eng.run_stats(s, 0, 512, cfg.pct)
+            del s
+            for a, b in zip(got[:3], ref[:3]):
+                assert np.array_equal(a, b)
+            assert got[3] == ref[3]
+        fut.result()
