@@ -1268,8 +1268,10 @@ gate_eval(DesignDev D, ChunkDev C, LevelArgs A) {
     if (lane == 0) it = atomicAdd(C.work + A.counter, 1u);
     it = __shfl_sync(0xffffffffu, it, 0);
     if (it >= items) break;
-    const int j = (int)(it / (unsigned)A.ntg);
-    const int tg = (int)(it % (unsigned)A.ntg);
+    // tile-group-major: the warps in flight share tile groups, so the fanin
+    // tiles one net feeds to several gates are read while they are in L2
+    const int j = (int)(it % (unsigned)A.n);
+    const int tg = (int)(it / (unsigned)A.n);
     const int g = __ldg(D.order + A.lo + j);
     const int k = K > 0 ? K : __ldg(D.gate_k + g);
     const int pin0 = __ldg(D.gate_pin + g);
