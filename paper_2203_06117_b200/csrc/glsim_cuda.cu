@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <charconv>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -713,7 +714,12 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     CK(cudaEventRecord(e->ev[1], e->st));
     // ---- K4: per level, one launch per fanin-count group (the launch
     // boundary between levels is the level barrier)
-    const int64_t warps = (int64_t)nregions;
+    // warps the item sizing assumes (GS_ITEM_WARPS: test hook that makes small
+    // designs take the coarse-item and tail-split paths of large ones)
+    static const int64_t item_warps = getenv("GS_ITEM_WARPS") ? atoll(getenv("GS_ITEM_WARPS")) : 0;
+    const int64_t warps = item_warps > 0 ? item_warps : (int64_t)nregions;
+    static const int tail_div = getenv("GS_TAIL_DIV") ? atoi(getenv("GS_TAIL_DIV")) : 2;
+    static const int tail_frac = getenv("GS_TAIL_FRAC") ? atoi(getenv("GS_TAIL_FRAC")) : 2;
     int nl = 0;
     for (int l = 0; l < D->L; ++l) {
       for (int gi = 0; gi < 5; ++gi) {
@@ -729,6 +735,26 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
         A.tpi = std::min(A.tpi, Tc);
         while ((int64_t)n * ((Tc + A.tpi - 1) / A.tpi) >= (int64_t(1) << 31)) A.tpi *= 2;
         A.ntg = (Tc + A.tpi - 1) / A.tpi;
+        // tail: about one head item's worth of tiles per warp, re-cut into
+        // items of tpi / tail_div tiles, so warps finish a launch close
+        // together; only where the column-aligned tail stays within 1 /
+        // tail_frac of the tiles (small items cost per-item setup and L2
+        // reuse).  Defaults from profiles/ab_tail.sh: C2 -3.0 %, C3 -0.7 %.
+        A.tpi2 = std::max(1, A.tpi / tail_div);
+        A.ntg2 = 0;
+        if (tail_div > 1 && A.tpi > 1 && A.ntg > 1) {
+          const int64_t need = std::min<int64_t>((int64_t)(A.ntg - 1) * A.tpi,
+                                                 (warps * A.tpi + n - 1) / n);
+          const int hg = (int)((Tc - need) / A.tpi);  // head groups (whole)
+          if ((int64_t)(Tc - hg * A.tpi) * tail_frac <= Tc) {
+            A.ntg2 = (Tc - hg * A.tpi + A.tpi2 - 1) / A.tpi2;
+            A.ntg = hg;
+          }
+          if ((int64_t)n * (A.ntg + A.ntg2) >= (int64_t(1) << 31)) {
+            A.ntg = (Tc + A.tpi - 1) / A.tpi;
+            A.ntg2 = 0;
+          }
+        }
         A.pct = pct;
         A.counter = l * 5 + gi;
         const int sm = e->sms;

@@ -139,7 +139,8 @@ struct StimDev {
 
 struct LevelArgs {
   int lo, n;                   // gates order[lo, lo+n)
-  int tpi, ntg;                // 128-tiles per item, tile groups per gate
+  int tpi, ntg;                // 128-tiles per item, tile groups per gate (head)
+  int tpi2, ntg2;              // the same for the tail tiles [ntg * tpi, Tc)
   int pct;
   int counter;                 // index into ChunkDev::work
 };
@@ -1262,7 +1263,8 @@ gate_eval(DesignDev D, ChunkDev C, LevelArgs A) {
   SM &S = reinterpret_cast<SM *>(smem_raw)[warp];
   const unsigned lane = lane_id();
   Region R = region_open(C, (unsigned long long)blockIdx.x * kEvalWarps + warp);
-  const unsigned items = (unsigned)A.n * (unsigned)A.ntg;
+  const unsigned head = (unsigned)A.n * (unsigned)A.ntg;
+  const unsigned items = head + (unsigned)A.n * (unsigned)A.ntg2;
   while (true) {
     unsigned it = 0;
     if (lane == 0) it = atomicAdd(C.work + A.counter, 1u);
@@ -1270,14 +1272,18 @@ gate_eval(DesignDev D, ChunkDev C, LevelArgs A) {
     if (it >= items) break;
     // tile-group-major: the warps in flight share tile groups, so the fanin
     // tiles one net feeds to several gates are read while they are in L2
-    const int j = (int)(it % (unsigned)A.n);
-    const int tg = (int)(it / (unsigned)A.n);
+    // head items of tpi tiles, then the tail in items of tpi2 < tpi tiles so
+    // the end of the launch drains in small pieces (guided self-scheduling)
+    const bool in_head = it < head;
+    const unsigned iq = in_head ? it : it - head;
+    const int j = (int)(iq % (unsigned)A.n);
+    const int tg = (int)(iq / (unsigned)A.n);
     const int g = __ldg(D.order + A.lo + j);
     const int k = K > 0 ? K : __ldg(D.gate_k + g);
     const int pin0 = __ldg(D.gate_pin + g);
     const unsigned long long lut = __ldg(D.gate_lut + g);
-    const int t_lo = tg * A.tpi;
-    const int t_hi = min(t_lo + A.tpi, C.Tc);
+    const int t_lo = in_head ? tg * A.tpi : A.ntg * A.tpi + tg * A.tpi2;
+    const int t_hi = min(t_lo + (in_head ? A.tpi : A.tpi2), C.Tc);
     int net[KM], arc[KM];
     TT ic[KM];
 #pragma unroll
