@@ -720,6 +720,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     const int64_t warps = item_warps > 0 ? item_warps : (int64_t)nregions;
     static const int tail_div = getenv("GS_TAIL_DIV") ? atoi(getenv("GS_TAIL_DIV")) : 2;
     static const int tail_frac = getenv("GS_TAIL_FRAC") ? atoi(getenv("GS_TAIL_FRAC")) : 2;
+    static const int tail_mult = getenv("GS_TAIL_MULT") ? atoi(getenv("GS_TAIL_MULT")) : 1;
     int nl = 0;
     for (int l = 0; l < D->L; ++l) {
       for (int gi = 0; gi < 5; ++gi) {
@@ -744,7 +745,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
         A.ntg2 = 0;
         if (tail_div > 1 && A.tpi > 1 && A.ntg > 1) {
           const int64_t need = std::min<int64_t>((int64_t)(A.ntg - 1) * A.tpi,
-                                                 (warps * A.tpi + n - 1) / n);
+                                                 (tail_mult * warps * A.tpi + n - 1) / n);
           const int hg = (int)((Tc - need) / A.tpi);  // head groups (whole)
           if ((int64_t)(Tc - hg * A.tpi) * tail_frac <= Tc) {
             A.ntg2 = (Tc - hg * A.tpi + A.tpi2 - 1) / A.tpi2;
