@@ -721,6 +721,8 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     static const int tail_div = getenv("GS_TAIL_DIV") ? atoi(getenv("GS_TAIL_DIV")) : 2;
     static const int tail_frac = getenv("GS_TAIL_FRAC") ? atoi(getenv("GS_TAIL_FRAC")) : 2;
     static const int tail_mult = getenv("GS_TAIL_MULT") ? atoi(getenv("GS_TAIL_MULT")) : 1;
+    static const int item_div = getenv("GS_ITEM_DIV") ? atoi(getenv("GS_ITEM_DIV")) : 4;
+    static const int item_cap = getenv("GS_ITEM_CAP") ? atoi(getenv("GS_ITEM_CAP")) : 8;
     int nl = 0;
     for (int l = 0; l < D->L; ++l) {
       for (int gi = 0; gi < 5; ++gi) {
@@ -732,7 +734,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
         A.n = n;
         // items of tpi tiles: enough items for dynamic balance, few enough
         // that per-item setup and work-counter atomics stay negligible
-        A.tpi = (int)std::max<int64_t>(1, std::min<int64_t>(8, (int64_t)n * Tc / (4 * warps)));
+        A.tpi = (int)std::max<int64_t>(1, std::min<int64_t>(item_cap, (int64_t)n * Tc / (item_div * warps)));
         A.tpi = std::min(A.tpi, Tc);
         while ((int64_t)n * ((Tc + A.tpi - 1) / A.tpi) >= (int64_t(1) << 31)) A.tpi *= 2;
         A.ntg = (Tc + A.tpi - 1) / A.tpi;
