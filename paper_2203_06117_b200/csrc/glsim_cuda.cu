@@ -722,7 +722,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     static const int tail_frac = getenv("GS_TAIL_FRAC") ? atoi(getenv("GS_TAIL_FRAC")) : 2;
     static const int tail_mult = getenv("GS_TAIL_MULT") ? atoi(getenv("GS_TAIL_MULT")) : 1;
     static const int item_div = getenv("GS_ITEM_DIV") ? atoi(getenv("GS_ITEM_DIV")) : 4;
-    static const int item_cap = getenv("GS_ITEM_CAP") ? atoi(getenv("GS_ITEM_CAP")) : 8;
+    static const int item_cap = getenv("GS_ITEM_CAP") ? atoi(getenv("GS_ITEM_CAP")) : 12;
     int nl = 0;
     for (int l = 0; l < D->L; ++l) {
       for (int gi = 0; gi < 5; ++gi) {
