@@ -1,15 +1,23 @@
-"""Benchmark: gate-cycle evaluations per second of the windowed re-simulation hot
-path on 1..8 B200 (one process per GPU), with roofline, CPU baseline and
-end-to-end numbers.  Prints ONE JSON line on rank 0.
+"""Benchmark: gate-cycle evaluations per second of the windowed re-simulation
+hot path on 1..8 B200 (one process per GPU), with roofline, CPU baseline,
+in-bench parity gate and end-to-end numbers.  Prints ONE JSON line on rank 0.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
-A step = one pass of the hot path over this rank's window shard of the config:
-K1 stimulus segmentation + one K4 gate-eval launch per logic level with the
-toggle/dwell reduction fused, the per-net sums accumulated on the device, and
-(N > 1) one NCCL all-reduce of those sums.  Work per GPU is fixed (weak
-scaling): rank r simulates windows [r*Wc, (r+1)*Wc) of the config's stimulus.
+Workload: at N = 1 the C3 roofline-study config -- 1M gates x
+100,000 cycle windows, the largest single-GPU config of BASELINE.json; at
+N > 1 the C4 config (10M gates), weak scaling: each rank simulates a fixed
+share of windows, the shards cut by ``distributed.shard_windows`` at equal
+shares of per-window input activity.
+
+A step = one pass of the hot path over the rank's windows: per window chunk
+K1 stimulus segmentation + one K4 gate-eval launch per (level, fanin group)
+with the toggle/dwell reduction fused, per-net sums accumulated on the device,
+and (N > 1) one NCCL all-reduce of those sums.  ``value`` has the stimulus
+already resident in HBM (generated there, bit-identical to synth.stimulus);
+``e2e`` takes it from pinned host memory through the C ABI every step
+(gs_stim_create: H2D + device validation) and reads the sums back.
 """
 
 import argparse
@@ -28,19 +36,20 @@ sys.path.insert(0, ROOT)
 
 METRIC = "gate-cycle evals/sec (whole box)"
 UNIT = "gate-cycle evals/s"
+C4_WINDOWS_PER_GPU = 16384
 
 
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--windows", type=int, default=0, help="windows per GPU (0 = config's)")
+    ap.add_argument("--config", default="", help="C2/C3/C4/C5-... (default C3 at N=1, C4 at N>1)")
+    ap.add_argument("--windows", type=int, default=0, help="windows per GPU (0 = the config's)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-windows", type=int, default=0,
-                    help="CPU baseline sample windows (0 = auto)")
+                    help="CPU baseline / parity sample windows (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -58,6 +67,36 @@ def peaks():
             return json.load(f)["hbm_gbs"], "measured (MEASURED_PEAKS.json)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def host_cpu():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def pick_config(args, world):
+    from paper_2203_06117_b200 import synth
+    name = args.config or ("C3" if world == 1 else "C4")
+    cfg = synth.config(name)
+    if args.windows:
+        per_gpu = args.windows
+    elif name == "C4":
+        per_gpu = C4_WINDOWS_PER_GPU
+    else:
+        per_gpu = cfg.windows
+    return cfg, per_gpu
+
+
+def cpu_sample_windows(args, cfg):
+    """Windows of the CPU baseline / parity sample: ~1e8 gate-windows."""
+    if args.cpu_windows:
+        return args.cpu_windows
+    return int(max(4, min(2048, 1.0e8 // cfg.gates)))
 
 
 # ---------------------------------------------------------------- clocks
@@ -114,66 +153,74 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- CPU legs
 
-def cpu_oracle_rate(cfg, design_arrays, windows, threads, chunk=256):
-    """The oracle port (reference algorithm in C + numpy, OpenMP) over windows
-    [0, windows) of the config, in window chunks (exact: windows are
-    independent) to bound host memory: (gate-cycle evals/s, seconds).  Timed:
-    the simulation and the stats reduction (inputs prepared beforehand, like
-    the GPU `value` leg)."""
+def oracle_run(cfg, model, w_lo, w_hi, threads):
+    """The reference algorithm on the host (oracle port: the reference's
+    windowing, count pass, store pass and dwell_sweep restated in C/numpy,
+    OpenMP) over absolute windows [w_lo, w_hi) of the config: (stats dict,
+    arena dict, seconds).  Timed: StimulusSet.build's windowing of the
+    per-input waveforms (WF:243-265, as the reference's Python loop), both
+    passes and compute_stats -- the reference's path from per-input
+    waveforms to per-net statistics."""
     from oracle import port
     from paper_2203_06117_b200 import synth
     port.build()
-    m = design_arrays
+    m = model
     d = port.Design.from_arrays(m.num_pis, m.order, m.level_starts, m.pin_off, m.pin_net,
                                 m.pin_ic, m.pin_arc, m.arc_rows, m.lut_off, m.lut_bits)
-    dt = 0.0
-    for a in range(0, windows, chunk):
-        b = min(windows, a + chunk)
-        s = synth.stimulus(cfg, a, b)
-        st = port.Stimulus.from_csr(s.pi_off, s.pi_times, s.pi_init, s.boundaries)
-        t0 = time.perf_counter()
-        arena = port.two_pass_simulate(d, st, pct=cfg.pct, threads=threads)
-        port.compute_stats(d, st, arena, threads=threads)
-        dt += time.perf_counter() - t0
-        del arena, st
-    return cfg.gates * windows / dt, dt
+    s = synth.stimulus(cfg, w_lo, w_hi)
+    t0 = time.perf_counter()
+    st = port.Stimulus.from_csr(s.pi_off, s.pi_times, s.pi_init, s.boundaries)
+    arena = port.two_pass_simulate(d, st, pct=cfg.pct, threads=threads)
+    stats = port.compute_stats(d, st, arena, threads=threads)
+    dt = time.perf_counter() - t0
+    return stats, arena, dt
 
 
-def run_reference_arm(args, cfg, rank, world):
-    """--impl reference: the reference algorithm (oracle port, all host cores)
-    on this config; rank 0 only."""
+def run_reference_arm(args, rank, world):
+    """--impl reference: the reference algorithm (oracle port, all host
+    cores) on this config's workload; rank 0 only, a bounded window sample
+    per step."""
     if rank != 0:
         return
     from paper_2203_06117_b200 import synth
+    cfg, per_gpu = pick_config(args, world)
     threads = os.cpu_count() or 1
-    sample = args.cpu_windows or 128
+    sample = cpu_sample_windows(args, cfg)
     m = synth.design(cfg)
-    rates = []
+    times = []
     for i in range(args.warmup + args.steps):
-        r, dt = cpu_oracle_rate(cfg, m, sample, threads)
+        lo = (i * sample) % max(1, per_gpu - sample + 1)
+        _, _, dt = oracle_run(cfg, m, lo, lo + sample, threads)
         if i >= args.warmup:
-            rates.append((r, dt))
-    v = statistics.median(r for r, _ in rates)
-    ms = statistics.median(dt for _, dt in rates) * 1e3
+            times.append(dt)
+    dt = statistics.median(times)
+    v = cfg.gates * sample / dt
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "impl": "reference",
-            "config": config_desc(cfg, sample),
+            "config": {**config_desc(cfg, per_gpu, world), "sample_windows_per_step": sample},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{cfg.name} design, windows [0,{sample}) per step: "
-                                       "count pass + store pass + dwell (oracle/port.py)"},
+                             "cpu": host_cpu(),
+                             "sample": f"{cfg.name} design, {sample} consecutive windows per "
+                                       "step: oracle/port.py (the reference's algorithm "
+                                       "restated in C + numpy, OpenMP; the reference itself is "
+                                       "numba and does not travel to the GPU box) -- "
+                                       "windowing, count + store pass, dwell sweep; rate "
+                                       "extrapolates linearly (windows are independent)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def config_desc(cfg, windows_per_gpu):
+def config_desc(cfg, windows_per_gpu, world):
     return {"workload": f"{cfg.name}: {cfg.description}", "gates": cfg.gates,
             "levels": cfg.levels, "inputs": cfg.num_inputs, "windows_per_gpu": windows_per_gpu,
-            "period_fs": cfg.period, "pathpulse_pct": cfg.pct, "delay_mode":
-            "averaged" if cfg.averaged else "full conditional",
-            "l2": "inputs larger than L2 (each step streams GBs of waveform/count arrays "
-                  "through HBM; no flush needed)"}
+            "windows_total": windows_per_gpu * world, "period_fs": cfg.period,
+            "pathpulse_pct": cfg.pct,
+            "delay_mode": "averaged" if cfg.averaged else "full conditional",
+            "parallelism": f"windows sharded x{world}" if world > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (each step streams tens of GB of waveform/count "
+                  "arrays through HBM; no flush needed)"}
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -190,28 +237,30 @@ def algorithmic_bytes(model, windows, input_toggles, output_toggles):
 def main():
     args = parse_args()
     rank, world, local = dist_env()
-    from paper_2203_06117_b200 import synth
-    cfg = synth.config(args.config)
     if args.impl == "reference":
-        return run_reference_arm(args, cfg, rank, world)
+        return run_reference_arm(args, rank, world)
 
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     import torch
     import torch.distributed as dist
-    from paper_2203_06117_b200 import _native, simcore
+    from paper_2203_06117_b200 import _native, distributed, synth
 
     torch.cuda.set_device(local)
     _native.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    Wr = args.windows or cfg.windows
-    w_lo, w_hi = rank * Wr, (rank + 1) * Wr
+    cfg, per_gpu = pick_config(args, world)
+    total = per_gpu * world
+    weights = _native.synth_window_counts(cfg, 0, total, local) + 1 if world > 1 else None
+    w_lo, w_hi = distributed.shard_windows(total, world, rank, weights)
+    Wr = w_hi - w_lo
     model = synth.design(cfg)
-    stim = synth.stimulus(cfg, w_lo, w_hi)
     N = model.num_nets
 
     stream = torch.cuda.Stream()
     dev = model.device()
-    dstim = _native.Stimulus(dev, stim)
+    dstim = _native.SynthStimulus(dev, cfg, w_lo, w_hi)   # resident in HBM
     eng = _native.Engine(dev, 0, stream.cuda_stream)
     acc = torch.zeros(3 * N + 3, dtype=torch.int64, device="cuda")
 
@@ -246,16 +295,14 @@ def main():
         clocks = sampler.stop()
         ms = e0.elapsed_time(e1)
         timing = eng.timing()
+        acc_value = acc.clone()
 
         # ---- end to end through the C ABI with host buffers: pinned host CSR
         # stimulus -> device (gs_stim_create), run, per-net sums -> host
-        pin = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
-               for k, v in (("off", stim.pi_off), ("t", stim.pi_times), ("i", stim.pi_init),
-                            ("b", stim.boundaries))}
         from paper_2203_06117_b200.waveform import StimulusSet
-        hstim = StimulusSet.from_csr(pin["b"].numpy(), pin["off"].numpy(), pin["t"].numpy(),
-                                     pin["i"].numpy())
-        h2d = sum(int(v.numel() * v.element_size()) for v in pin.values())
+        hb, hoff, htimes, hinit = dstim.download(pinned=True)
+        hstim = StimulusSet.from_csr(hb, hoff, htimes, hinit)
+        h2d = hb.nbytes + hoff.nbytes + htimes.nbytes + hinit.nbytes
         d2h = acc.numel() * 8
         host_acc = torch.empty(acc.numel(), dtype=torch.int64).pin_memory()
         if world > 1:
@@ -283,8 +330,6 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         with ThreadPoolExecutor(1) as ex:
-            # untimed: one overlapped step, so the stimulus pool holds two
-            # stimuli (its growth is a one-off, not a per-step cost)
             fut = ex.submit(_native.Stimulus, dev, hstim)
             s_w = _native.Stimulus(dev, hstim)
             step(s_w)
@@ -305,6 +350,8 @@ def main():
                 del s_i
             t1 = time.perf_counter()
         e2e_ms = 1e3 * (t1 - t0) / K
+        e2e_same = bool(torch.equal(host_acc, acc_value.cpu()))
+        del hstim, hb, hoff, htimes, hinit
 
     # max over ranks
     tm = torch.tensor([ms, e2e_ms, eval_ms], dtype=torch.float64, device="cuda")
@@ -312,12 +359,12 @@ def main():
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
     ms, e2e_ms, eval_ms = tm.tolist()
     ms_step = ms / args.steps
-    units = cfg.gates * Wr * world
+    units = cfg.gates * total
     value = units / (ms_step / 1e3)
     e2e_value = units / (e2e_ms / 1e3)
 
-    # roofline of K4 (this rank's work; identical every step).  Toggle totals
-    # come from this rank's own per-net counts: n_in = sum over pins of the
+    # roofline of K4 on this rank's windows (identical every step).  Toggle
+    # totals from this rank's per-net counts: n_in = sum over pins of the
     # driving net's toggles, n_out = gate-net toggles.
     acc.zero_()
     eng.run_stats_device(dstim, 0, Wr, cfg.pct, acc.data_ptr())
@@ -333,30 +380,48 @@ def main():
     prof = os.path.join(ROOT, "profiles", "k4_traffic.json")
     if os.path.exists(prof):
         try:
-            pj = json.load(open(prof))
-            for ent in (pj if isinstance(pj, list) else [pj]):
+            for ent in json.load(open(prof)):
                 if ent.get("config") == cfg.name and ent.get("windows") == Wr:
                     traffic = ent.get("dram_bytes_per_launch")
         except Exception:
             pass
 
-    cpu = None
+    # parity gate and CPU baseline (rank 0, N = 1): the oracle on a sample of
+    # this run's windows against the device's per-net sums for the same
+    # windows
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        sample = args.cpu_windows or 2048
-        r, dt = cpu_oracle_rate(cfg, model, sample, threads)
-        cpu = {"value": r, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{cfg.name} design, windows [0,{sample}) in chunks of 256: oracle "
-                         f"port (reference algorithm) count+store passes + dwell on {threads} "
-                         f"host threads, {dt:.1f} s of CPU work"}
+        S = min(cpu_sample_windows(args, cfg), Wr)
+        ref, arena, dt = oracle_run(cfg, model, w_lo, w_lo + S, threads)
+        got = eng.run_stats(dstim, 0, S, cfg.pct)
+        tot = (int(arena["filtered"].sum()), int(arena["ic_filtered"].sum()),
+               int(arena["discarded"].sum()))
+        t0g = (int(ref["duration"]) - got[0])
+        ok = (np.array_equal(got[0], ref["t1"]) and np.array_equal(t0g, ref["t0"])
+              and np.array_equal(got[1], ref["tc"]) and np.array_equal(got[2], ref["ig"])
+              and tuple(got[3]) == tot)
+        parity = {"result": "ok" if ok else "MISMATCH", "windows": [w_lo, w_lo + S],
+                  "nets": N, "checked": "per-net T0/T1/TC/IG and filtered/ic_filtered/"
+                  "discarded totals, device run vs oracle/port.py, bit-exact",
+                  "e2e_sums_equal_value_sums": e2e_same}
+        r = cfg.gates * S / dt
+        cpu = {"value": r, "unit": UNIT, "cores": threads, "kind": "port", "cpu": host_cpu(),
+               "sample": f"{cfg.name} design, windows [{w_lo},{w_lo + S}) ({S} of {Wr}; "
+                         f"linear extrapolation, windows are independent): oracle/port.py, "
+                         f"the reference algorithm restated in C + numpy with OpenMP (the "
+                         f"numba reference does not travel to the GPU box) -- windowing, "
+                         f"count + store pass, dwell sweep -- on {threads} host threads, "
+                         f"{dt:.1f} s"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "int64", "data": "synthetic (counter-based RNG stimulus, random-init "
-                                          "design of the config's shape)",
-                "config": {**config_desc(cfg, Wr), "parallelism": f"windows sharded x{world}"},
+                "dtype": "int64", "data": "synthetic (counter-based RNG stimulus generated "
+                                          "on the device, random-init design of the "
+                                          "config's shape)",
+                "config": config_desc(cfg, per_gpu, world),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                              "frac": achieved / hbm, "traffic": traffic,
                              "kernel": "gate_eval (K4)", "peak_source": peak_src,
@@ -374,9 +439,15 @@ def main():
                 "activity": {"input_toggles_per_gw": in_tog / (cfg.gates * Wr),
                              "output_toggles_per_gw": out_tog / (cfg.gates * Wr),
                              "chunks_per_step": timing["chunks"]}}
+        if world > 1:
+            line["shards"] = "distributed.shard_windows over per-window input activity"
+        if parity is not None:
+            line["parity"] = parity
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
+        if parity is not None and parity["result"] != "ok":
+            sys.exit(3)
     if world > 1:
         dist.destroy_process_group()
 

@@ -132,6 +132,33 @@ int gs_design_destroy(gs_design *d);
 int gs_stim_create(gs_design *d, const gs_stim_desc *desc, gs_stim **out);
 int gs_stim_destroy(gs_stim *s);
 
+/* Synthetic benchmark stimulus, generated on the device (no reference
+ * counterpart: the benchmark configs of SURVEY §8(d); bit-identical to the
+ * package's synth.stimulus_arrays).  Input p toggles in absolute window w iff
+ * (splitmix64(seed<<56 ^ p<<32 ^ w) >> 11) < thr (thr = ceil(alpha * 2^53)),
+ * at w*period + lo + splitmix64(h1 ^ 0xD1B54A32D192ED03) % span; inputs
+ * [0, num_ppis) use the ppi_* parameters.  The stimulus' window 0 is w_lo
+ * (initial values carry the toggle parity of windows [0, w_lo)). */
+typedef struct gs_synth_desc {
+  int64_t num_pis, num_ppis;
+  uint64_t seed;
+  int64_t period;
+  uint64_t ppi_thr, pi_thr;
+  int64_t ppi_lo, ppi_span, pi_lo, pi_span;
+  int64_t w_lo, w_hi;
+} gs_synth_desc;
+int gs_stim_synth(gs_design *d, const gs_synth_desc *desc, gs_stim **out);
+/* per-window input toggles of the synthetic stimulus over [w_lo, w_hi) on
+ * `device`, into counts [w_hi - w_lo] (the weights window shards are balanced
+ * by, without generating the stimulus) */
+int gs_synth_window_counts(const gs_synth_desc *desc, int device, int64_t *counts);
+/* windows and input toggles of a stimulus */
+int gs_stim_sizes(const gs_stim *s, int64_t *num_windows, int64_t *num_toggles);
+/* copy a CSR stimulus back to host arrays: boundaries [W+1], pi_off [P+1],
+ * pi_times [num_toggles], pi_init [P] (any may be NULL) */
+int gs_stim_download(const gs_stim *s, int64_t *boundaries, int64_t *pi_off, int64_t *pi_times,
+                     uint8_t *pi_init);
+
 /* ---- engine ------------------------------------------------------------ */
 /* mem_budget: bytes of device memory the engine may use for its window-chunk
  * workspace (0 = 75% of free memory).  stream: a cudaStream_t (NULL = the

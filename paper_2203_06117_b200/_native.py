@@ -40,6 +40,13 @@ class StimDesc(C.Structure):
                 ("counts", _i64p), ("initials", _u8p)]
 
 
+class SynthDesc(C.Structure):
+    _fields_ = [("num_pis", C.c_int64), ("num_ppis", C.c_int64), ("seed", C.c_uint64),
+                ("period", C.c_int64), ("ppi_thr", C.c_uint64), ("pi_thr", C.c_uint64),
+                ("ppi_lo", C.c_int64), ("ppi_span", C.c_int64), ("pi_lo", C.c_int64),
+                ("pi_span", C.c_int64), ("w_lo", C.c_int64), ("w_hi", C.c_int64)]
+
+
 class StatsOut(C.Structure):
     _fields_ = [("t1", _i64p), ("tc", _i64p), ("ig", _i64p), ("totals", C.c_int64 * 3)]
 
@@ -82,6 +89,10 @@ SIGNATURES = {
     "gs_design_destroy": (C.c_int, [C.c_void_p]),
     "gs_stim_create": (C.c_int, [C.c_void_p, C.POINTER(StimDesc), C.POINTER(C.c_void_p)]),
     "gs_stim_destroy": (C.c_int, [C.c_void_p]),
+    "gs_stim_synth": (C.c_int, [C.c_void_p, C.POINTER(SynthDesc), C.POINTER(C.c_void_p)]),
+    "gs_synth_window_counts": (C.c_int, [C.POINTER(SynthDesc), C.c_int, _i64p]),
+    "gs_stim_sizes": (C.c_int, [C.c_void_p, _i64p, _i64p]),
+    "gs_stim_download": (C.c_int, [C.c_void_p, _i64p, _i64p, _i64p, _u8p]),
     "gs_engine_create": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(C.c_void_p)]),
     "gs_engine_destroy": (C.c_int, [C.c_void_p]),
     "gs_run_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
@@ -412,6 +423,62 @@ class Stimulus:
         self.design = design
         self.num_windows = b.size - 1
         self._fin = weakref.finalize(self, lib.gs_stim_destroy, h)
+
+
+def _synth_desc(cfg, w_lo, w_hi):
+    import math
+
+    def thr(a):  # u < alpha, as the integer test (h1 >> 11) < ceil(alpha * 2^53)
+        return math.ceil(a * float(1 << 53))
+    return SynthDesc(num_pis=cfg.num_inputs, num_ppis=cfg.ppis, seed=cfg.seed,
+                     period=cfg.period, ppi_thr=thr(cfg.ppi_alpha), pi_thr=thr(cfg.pi_alpha),
+                     ppi_lo=cfg.ppi_lo, ppi_span=cfg.ppi_hi - cfg.ppi_lo, pi_lo=cfg.pi_lo,
+                     pi_span=cfg.pi_hi - cfg.pi_lo, w_lo=int(w_lo), w_hi=int(w_hi))
+
+
+def synth_window_counts(cfg, w_lo, w_hi, device=None):
+    """Per-window input toggles of a config's synthetic stimulus over
+    [w_lo, w_hi), counted on the device (``gs_synth_window_counts``)."""
+    out = np.empty(int(w_hi) - int(w_lo), dtype=np.int64)
+    d = _synth_desc(cfg, w_lo, w_hi)
+    _check(load().gs_synth_window_counts(C.byref(d), current_device() if device is None
+                                         else int(device), _p64(out)))
+    return out
+
+
+class SynthStimulus(Stimulus):
+    """A benchmark config's stimulus generated on the device
+    (``gs_stim_synth``; identical to :func:`synth.stimulus` for the same
+    window range)."""
+
+    def __init__(self, design, cfg, w_lo, w_hi):  # noqa: D107 (no super().__init__: no host arrays)
+        lib = load()
+        d = _synth_desc(cfg, w_lo, w_hi)
+        h = C.c_void_p()
+        _check(lib.gs_stim_synth(design.handle, C.byref(d), C.byref(h)))
+        self.handle = h
+        self.design = design
+        self.num_windows = int(w_hi) - int(w_lo)
+        self._fin = weakref.finalize(self, lib.gs_stim_destroy, h)
+
+    def download(self, pinned=False):
+        """Host CSR arrays (boundaries, pi_off, pi_times, pi_init); page-locked
+        (torch pinned memory) when ``pinned``."""
+        lib = load()
+        W, T = C.c_int64(), C.c_int64()
+        _check(lib.gs_stim_sizes(self.handle, C.byref(W), C.byref(T)))
+        P = self.design.num_pis
+        shapes = ((W.value + 1, np.int64), (P + 1, np.int64), (T.value, np.int64), (P, np.uint8))
+        if pinned:
+            import torch
+            arrs = [torch.empty(n, dtype=torch.int64 if t is np.int64 else torch.uint8)
+                    .pin_memory().numpy() for n, t in shapes]
+        else:
+            arrs = [np.empty(n, dtype=t) for n, t in shapes]
+        b, off, tm, ini = arrs
+        _check(lib.gs_stim_download(self.handle, _p64(b), _p64(off), _p64(tm) if tm.size else None,
+                                    _p8(ini) if ini.size else None))
+        return b, off, tm, ini
 
 
 class Engine:

@@ -14,6 +14,8 @@
 
 #include "glsim_cuda.h"
 #include "kernels.cuh"
+#include "kernels_lean.cuh"
+#include "synth.cuh"
 #include "vcd_reader.h"
 #include "sdf_reader.h"
 
@@ -473,22 +475,37 @@ namespace {
 
 // Per gate_eval instantiation: opt in to its dynamic shared memory (per-warp
 // tile state, above the 48 KB static limit) and size its persistent grid from
-// its own occupancy.  Output regions are indexed by (CTA, warp), so every
+// its own occupancy.  The opt-in is a per-device function attribute, so it is
+// cached per device.  Output regions are indexed by (CTA, warp), so every
 // launch of a chunk shares the region array sized by the largest grid.
+constexpr int kMaxDevices = 64;
+
+template <typename F>
+int kernel_grid(F kernel, size_t smem, int sms, int *cache, int *grid) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return fail(GS_ERR_ARG, "device index out of range");
+  if (!cache[dev]) {
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kEvalThreads, smem));
+    cache[dev] = std::max(1, occ);
+  }
+  *grid = sms * cache[dev];
+  return GS_OK;
+}
+
 template <typename TS, typename TT, int MODE, int K, bool P100>
 int eval_grid(int sms, int *grid) {
-  static int cached = 0;
-  if (!cached) {
-    const size_t smem = eval_smem_bytes<TS, TT, K>();
-    CK(cudaFuncSetAttribute(gate_eval<TS, TT, MODE, K, P100>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gate_eval<TS, TT, MODE, K, P100>,
-                                                     kEvalThreads, smem));
-    cached = std::max(1, occ);
-  }
-  *grid = sms * cached;
-  return GS_OK;
+  static int cache[kMaxDevices] = {};
+  return kernel_grid(gate_eval<TS, TT, MODE, K, P100>, eval_smem_bytes<TS, TT, K>(), sms, cache,
+                     grid);
+}
+
+template <int MODE, int K, bool P100>
+int lean_grid(int sms, int *grid) {
+  static int cache[kMaxDevices] = {};
+  return kernel_grid(gate_eval_lean<MODE, K, P100>, lean_smem_bytes<K>(), sms, cache, grid);
 }
 
 template <typename TS, typename TT, int MODE, int K, bool P100>
@@ -502,20 +519,31 @@ int launch_eval(int sms, cudaStream_t st, const DesignDev &Dd, const ChunkDev &C
   return GS_OK;
 }
 
+template <int MODE, int K, bool P100>
+int launch_lean(int sms, cudaStream_t st, const DesignDev &Dd, const ChunkDev &C,
+                const LevelArgs &A, int max_grid) {
+  int grid = 0;
+  TRY((lean_grid<MODE, K, P100>(sms, &grid)));
+  grid = std::min(grid, max_grid);
+  gate_eval_lean<MODE, K, P100><<<grid, kEvalThreads, lean_smem_bytes<K>(), st>>>(Dd, C, A);
+  CK(cudaGetLastError());
+  return GS_OK;
+}
+
 // largest persistent grid any kernel of a run may use (sizes the regions)
 template <typename TS, int MODE>
 int grid_size(gs_engine *e, bool narrow, bool p100, int *ncta) {
   int g = 0, best = 0;
   if (narrow && p100) {
-    TRY((eval_grid<TS, unsigned, MODE, 1, true>(e->sms, &g))); best = std::max(best, g);
-    TRY((eval_grid<TS, unsigned, MODE, 2, true>(e->sms, &g))); best = std::max(best, g);
-    TRY((eval_grid<TS, unsigned, MODE, 3, true>(e->sms, &g))); best = std::max(best, g);
-    TRY((eval_grid<TS, unsigned, MODE, 4, true>(e->sms, &g))); best = std::max(best, g);
+    TRY((lean_grid<MODE, 1, true>(e->sms, &g))); best = std::max(best, g);
+    TRY((lean_grid<MODE, 2, true>(e->sms, &g))); best = std::max(best, g);
+    TRY((lean_grid<MODE, 3, true>(e->sms, &g))); best = std::max(best, g);
+    TRY((lean_grid<MODE, 4, true>(e->sms, &g))); best = std::max(best, g);
   } else if (narrow) {
-    TRY((eval_grid<TS, unsigned, MODE, 1, false>(e->sms, &g))); best = std::max(best, g);
-    TRY((eval_grid<TS, unsigned, MODE, 2, false>(e->sms, &g))); best = std::max(best, g);
-    TRY((eval_grid<TS, unsigned, MODE, 3, false>(e->sms, &g))); best = std::max(best, g);
-    TRY((eval_grid<TS, unsigned, MODE, 4, false>(e->sms, &g))); best = std::max(best, g);
+    TRY((lean_grid<MODE, 1, false>(e->sms, &g))); best = std::max(best, g);
+    TRY((lean_grid<MODE, 2, false>(e->sms, &g))); best = std::max(best, g);
+    TRY((lean_grid<MODE, 3, false>(e->sms, &g))); best = std::max(best, g);
+    TRY((lean_grid<MODE, 4, false>(e->sms, &g))); best = std::max(best, g);
   }
   TRY((eval_grid<TS, long long, MODE, 0, false>(e->sms, &g))); best = std::max(best, g);
   int o = 0;
@@ -558,7 +586,8 @@ int ensure_data(gs_engine *e, int64_t bytes) {
   if (e->data_bytes >= bytes) return GS_OK;
   dfree(e->data);
   e->data_bytes = 0;
-  CK(cudaMalloc(&e->data, (size_t)bytes));
+  // 64 bytes of slack: bulk copies of a segment round its end up to 16 bytes
+  CK(cudaMalloc(&e->data, (size_t)bytes + 64));
   e->data_bytes = bytes;
   return GS_OK;
 }
@@ -762,15 +791,15 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
         A.counter = l * 5 + gi;
         const int sm = e->sms;
         if (narrow && p100 && gi < 4) {
-          if (gi == 0) TRY((launch_eval<TS, unsigned, MODE, 1, true>(sm, e->st, Dd, C, A, ncta)));
-          if (gi == 1) TRY((launch_eval<TS, unsigned, MODE, 2, true>(sm, e->st, Dd, C, A, ncta)));
-          if (gi == 2) TRY((launch_eval<TS, unsigned, MODE, 3, true>(sm, e->st, Dd, C, A, ncta)));
-          if (gi == 3) TRY((launch_eval<TS, unsigned, MODE, 4, true>(sm, e->st, Dd, C, A, ncta)));
+          if (gi == 0) TRY((launch_lean<MODE, 1, true>(sm, e->st, Dd, C, A, ncta)));
+          if (gi == 1) TRY((launch_lean<MODE, 2, true>(sm, e->st, Dd, C, A, ncta)));
+          if (gi == 2) TRY((launch_lean<MODE, 3, true>(sm, e->st, Dd, C, A, ncta)));
+          if (gi == 3) TRY((launch_lean<MODE, 4, true>(sm, e->st, Dd, C, A, ncta)));
         } else if (narrow && gi < 4) {
-          if (gi == 0) TRY((launch_eval<TS, unsigned, MODE, 1, false>(sm, e->st, Dd, C, A, ncta)));
-          if (gi == 1) TRY((launch_eval<TS, unsigned, MODE, 2, false>(sm, e->st, Dd, C, A, ncta)));
-          if (gi == 2) TRY((launch_eval<TS, unsigned, MODE, 3, false>(sm, e->st, Dd, C, A, ncta)));
-          if (gi == 3) TRY((launch_eval<TS, unsigned, MODE, 4, false>(sm, e->st, Dd, C, A, ncta)));
+          if (gi == 0) TRY((launch_lean<MODE, 1, false>(sm, e->st, Dd, C, A, ncta)));
+          if (gi == 1) TRY((launch_lean<MODE, 2, false>(sm, e->st, Dd, C, A, ncta)));
+          if (gi == 2) TRY((launch_lean<MODE, 3, false>(sm, e->st, Dd, C, A, ncta)));
+          if (gi == 3) TRY((launch_lean<MODE, 4, false>(sm, e->st, Dd, C, A, ncta)));
         } else {
           TRY((launch_eval<TS, long long, MODE, 0, false>(sm, e->st, Dd, C, A, ncta)));
         }
@@ -967,6 +996,133 @@ int gs_stim_destroy(gs_stim *s) {
   cudaSetDevice(s->d->device);
   s->release();
   delete s;
+  return GS_OK;
+}
+
+static SynthArgs synth_args(const gs_synth_desc *sd) {
+  SynthArgs A;
+  A.P = (int)sd->num_pis;
+  A.ppis = (int)sd->num_ppis;
+  A.seed = sd->seed;
+  A.ppi_thr = sd->ppi_thr;
+  A.pi_thr = sd->pi_thr;
+  A.period = sd->period;
+  A.ppi_lo = sd->ppi_lo;
+  A.ppi_span = sd->ppi_span;
+  A.pi_lo = sd->pi_lo;
+  A.pi_span = sd->pi_span;
+  A.w_lo = sd->w_lo;
+  A.w_hi = sd->w_hi;
+  return A;
+}
+
+static int synth_check(const gs_synth_desc *sd) {
+  if (sd->num_pis < 0 || sd->num_pis > INT32_MAX) return fail(GS_ERR_ARG, "num_pis out of range");
+  if (sd->num_ppis < 0 || sd->num_ppis > sd->num_pis) return fail(GS_ERR_ARG, "num_ppis out of range");
+  if (sd->period <= 0) return fail(GS_ERR_ARG, "window period must be positive");
+  if (sd->w_lo < 0 || sd->w_hi <= sd->w_lo) return fail(GS_ERR_ARG, "need a non-empty window range");
+  if (sd->ppi_lo < 0 || sd->pi_lo < 0 || sd->ppi_span < 0 || sd->pi_span < 0 ||
+      sd->ppi_lo + std::max<int64_t>(sd->ppi_span, 1) > sd->period ||
+      sd->pi_lo + std::max<int64_t>(sd->pi_span, 1) > sd->period)
+    return fail(GS_ERR_ARG, "toggle offsets must lie inside the window");
+  if (sd->w_hi > INT64_MAX / sd->period - 1) return fail(GS_ERR_ARG, "window range overflows int64 time");
+  return GS_OK;
+}
+
+int gs_synth_window_counts(const gs_synth_desc *sd, int device, int64_t *counts) {
+  if (!sd || !counts) return fail(GS_ERR_ARG, "null synthetic-stimulus argument");
+  TRY(synth_check(sd));
+  TRY(use_device(device));
+  const int64_t W = sd->w_hi - sd->w_lo;
+  long long *c = nullptr;
+  TRY(dalloc(&c, (size_t)W));
+  const SynthArgs A = synth_args(sd);
+  synth_window_counts<<<(int)std::min<int64_t>((W + 255) / 256, 8192), 256>>>(A, c);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpy(counts, c, sizeof(long long) * W, cudaMemcpyDeviceToHost);
+  dfree(c);
+  if (e != cudaSuccess) return fail(GS_ERR_CUDA, cudaGetErrorString(e));
+  return GS_OK;
+}
+
+int gs_stim_synth(gs_design *d, const gs_synth_desc *sd, gs_stim **out) {
+  if (!d || !sd || !out) return fail(GS_ERR_ARG, "null synthetic-stimulus argument");
+  *out = nullptr;
+  if (sd->num_pis != d->P) return fail(GS_ERR_ARG, "stimulus input count != design inputs");
+  TRY(synth_check(sd));
+  const int64_t P = sd->num_pis, W = sd->w_hi - sd->w_lo;
+  gs_stim *S = new gs_stim();
+  S->d = d;
+  S->P = (int)P;
+  S->W = W;
+  S->csr = true;
+  S->max_wlen = sd->period;
+  S->wide = sd->period > (int64_t)0xFFFFFFFFll;
+  long long *cnt = nullptr;
+  int rc = [&]() -> int {
+    TRY(use_device(d->device));
+    TRY(pool_ready(d->device));
+    TRY(upload_stream(d->device, &S->us));
+    cudaStream_t us = S->us;
+    const SynthArgs A = synth_args(sd);
+    CK(cudaMallocAsync((void **)&S->bnd, sizeof(long long) * (W + 1), us));
+    CK(cudaMallocAsync((void **)&S->pi_off, sizeof(long long) * (P + 1), us));
+    CK(cudaMallocAsync((void **)&S->pi_init, std::max<int64_t>(P, 1), us));
+    CK(cudaMallocAsync((void **)&cnt, sizeof(long long) * std::max<int64_t>(P, 1), us));
+    synth_bounds<<<(int)std::min<int64_t>((W + 256) / 256, 4096), 256, 0, us>>>(S->bnd, sd->w_lo, W,
+                                                                                  sd->period);
+    CK(cudaGetLastError());
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((P + 7) / 8, 16384));
+    std::vector<long long> h(P + 1, 0);
+    if (P) {
+      synth_count<<<blocks, 256, 0, us>>>(A, cnt, S->pi_init);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(h.data() + 1, cnt, sizeof(long long) * P, cudaMemcpyDeviceToHost, us));
+      CK(cudaStreamSynchronize(us));
+    }
+    for (int64_t p = 0; p < P; ++p) h[p + 1] += h[p];
+    S->n_toggles = h[P];
+    CK(cudaMemcpyAsync(S->pi_off, h.data(), sizeof(long long) * (P + 1), cudaMemcpyHostToDevice, us));
+    CK(cudaMallocAsync((void **)&S->pi_times, sizeof(long long) * std::max<int64_t>(S->n_toggles, 1), us));
+    if (P) {
+      synth_fill<<<blocks, 256, 0, us>>>(A, S->pi_off, S->pi_times);
+      CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(us));
+    return GS_OK;
+  }();
+  if (cnt) cudaFreeAsync(cnt, S->us);
+  if (rc != GS_OK) {
+    S->release();
+    delete S;
+    return rc;
+  }
+  *out = S;
+  return GS_OK;
+}
+
+int gs_stim_sizes(const gs_stim *s, int64_t *num_windows, int64_t *num_toggles) {
+  if (!s) return fail(GS_ERR_ARG, "null stimulus");
+  if (num_windows) *num_windows = s->W;
+  if (num_toggles) *num_toggles = s->n_toggles;
+  return GS_OK;
+}
+
+int gs_stim_download(const gs_stim *s, int64_t *boundaries, int64_t *pi_off, int64_t *pi_times,
+                     uint8_t *pi_init) {
+  if (!s) return fail(GS_ERR_ARG, "null stimulus");
+  if (!s->csr) return fail(GS_ERR_ARG, "only CSR stimuli can be downloaded");
+  TRY(use_device(s->d->device));
+  cudaStream_t us = s->us;
+  if (boundaries)
+    CK(cudaMemcpyAsync(boundaries, s->bnd, sizeof(long long) * (s->W + 1), cudaMemcpyDeviceToHost, us));
+  if (pi_off)
+    CK(cudaMemcpyAsync(pi_off, s->pi_off, sizeof(long long) * (s->P + 1), cudaMemcpyDeviceToHost, us));
+  if (pi_times && s->n_toggles)
+    CK(cudaMemcpyAsync(pi_times, s->pi_times, sizeof(long long) * s->n_toggles,
+                       cudaMemcpyDeviceToHost, us));
+  if (pi_init && s->P) CK(cudaMemcpyAsync(pi_init, s->pi_init, s->P, cudaMemcpyDeviceToHost, us));
+  CK(cudaStreamSynchronize(us));
   return GS_OK;
 }
 
