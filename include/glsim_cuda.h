@@ -165,6 +165,11 @@ int gs_stim_download(const gs_stim *s, int64_t *boundaries, int64_t *pi_off, int
  * engine's own stream). */
 int gs_engine_create(gs_design *d, int64_t mem_budget, void *stream, gs_engine **out);
 int gs_engine_destroy(gs_engine *e);
+/* K4 work-item sizing (no reference counterpart; tuning and tests): the
+ * number of workers items are sized for (0 = the launch's own grid), the
+ * divisor the tail items are re-cut by (1 = no tail re-cut) and the largest
+ * tail share 1/tail_frac of a launch's columns.  Results never depend on it. */
+int gs_engine_set_items(gs_engine *e, int64_t workers, int tail_div, int tail_frac);
 
 /* Stats run over windows [w_lo, w_hi): K1 stim_segment + per level K4
  * gate_eval with the dwell/toggle reduction fused (replaces count_pass +

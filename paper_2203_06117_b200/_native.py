@@ -95,6 +95,7 @@ SIGNATURES = {
     "gs_stim_download": (C.c_int, [C.c_void_p, _i64p, _i64p, _i64p, _u8p]),
     "gs_engine_create": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(C.c_void_p)]),
     "gs_engine_destroy": (C.c_int, [C.c_void_p]),
+    "gs_engine_set_items": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_int]),
     "gs_run_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
                                C.POINTER(StatsOut)]),
     "gs_run_arena": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
@@ -492,6 +493,11 @@ class Engine:
         self.handle = h
         self.design = design
         self._fin = weakref.finalize(self, lib.gs_engine_destroy, h)
+
+    def set_items(self, workers=0, tail_div=2, tail_frac=2):
+        """K4 work-item sizing (``gs_engine_set_items``); results never depend on it."""
+        _check(load().gs_engine_set_items(self.handle, int(workers), int(tail_div),
+                                          int(tail_frac)))
 
     def run_stats(self, stim, w_lo, w_hi, pct):
         """Stats over [w_lo, w_hi): (t1, tc, ig [N] int64, totals (filt, icf, disc))."""

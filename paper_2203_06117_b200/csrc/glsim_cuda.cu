@@ -442,7 +442,11 @@ struct gs_engine {
   unsigned char *a_init = nullptr;
   int64_t a_buf_cap = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  int64_t chunk_hint = 0;
+  int64_t chunk_hint[2] = {0, 0};   // per mode family: stats, arena
+  // work-item sizing (gs_engine_set_items): workers assumed (0 = the grid),
+  // tail re-cut divisor (1 = none), tail share limit
+  int64_t item_workers = 0;
+  int tail_div = 2, tail_frac = 2;
   gs_timing last{};
 
   void release_meta() { dfree(cnt); dfree(tbase); dfree(init); dfree(wlen32); meta_windows = 0; }
@@ -593,9 +597,53 @@ int ensure_data(gs_engine *e, int64_t bytes) {
 }
 
 int64_t meta_bytes_per_window(const gs_design *d, bool arena) {
-  int64_t b = (int64_t)d->N * 4 + (int64_t)d->N * (8 / kTile + 4 / 32) + d->N / 8 + 1;
+  // cnt (4 B), tbase (8 B per 128-window tile), init bits (4 B per 32
+  // windows) per net-window, plus the window length
+  int64_t b = (int64_t)d->N * 4 + ((int64_t)d->N * 8 + kTile - 1) / kTile +
+              ((int64_t)d->N * 4 + 31) / 32 + 4;
   if (arena) b += (int64_t)d->G * (6 * 8 + 1);
   return b;
+}
+
+// Work-item sizing of a K4 launch over n gates x `units` column units
+// (tiles or super-tiles): head items of tpi units -- enough items for dynamic
+// balance over `workers` (4 per worker), few enough that per-item setup and
+// work-counter atomics stay negligible (at most `cap` units) -- then, where
+// the column-aligned tail stays within 1 / tail_frac of the units, about one
+// head item per worker re-cut into items of tpi / tail_div units, so the
+// workers of a launch finish close together (guided self-scheduling;
+// profiles/ab_tail.sh, round 1: C2 -3.0 %, C3 -0.7 %).
+constexpr int kItemCap = 12;   // tiles per item (profiles/ab_items_r01.log)
+constexpr int kItemDiv = 4;
+
+struct ItemPlan {
+  int tpi, ntg, tpi2, ntg2;
+};
+
+ItemPlan plan_items(int64_t n, int units, int64_t workers, int cap, int tail_div, int tail_frac) {
+  ItemPlan P;
+  workers = std::max<int64_t>(1, workers);
+  cap = std::max(1, cap);
+  P.tpi = (int)std::max<int64_t>(1, std::min<int64_t>(cap, n * units / (kItemDiv * workers)));
+  P.tpi = std::min(P.tpi, std::max(1, units));
+  while (n * ((units + P.tpi - 1) / P.tpi) >= (int64_t(1) << 31)) P.tpi *= 2;
+  P.ntg = (units + P.tpi - 1) / P.tpi;
+  P.tpi2 = std::max(1, P.tpi / std::max(1, tail_div));
+  P.ntg2 = 0;
+  if (tail_div > 1 && P.tpi > 1 && P.ntg > 1) {
+    const int64_t need = std::min<int64_t>((int64_t)(P.ntg - 1) * P.tpi,
+                                           (workers * P.tpi + n - 1) / n);
+    const int hg = (int)((units - need) / P.tpi);  // head groups (whole)
+    if ((int64_t)(units - hg * P.tpi) * std::max(1, tail_frac) <= units) {
+      P.ntg2 = (units - hg * P.tpi + P.tpi2 - 1) / P.tpi2;
+      P.ntg = hg;
+    }
+    if (n * (P.ntg + P.ntg2) >= (int64_t(1) << 31)) {
+      P.ntg = (units + P.tpi - 1) / P.tpi;
+      P.ntg2 = 0;
+    }
+  }
+  return P;
 }
 
 struct RunOut {
@@ -634,9 +682,11 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
   const int64_t pi_words = s->csr ? s->n_toggles : 0;
   const int64_t pi_bytes = round_up(pi_words * (int64_t)sizeof(TS), 256);
   const int64_t total = w_hi - w_lo;
-  // initial chunk: metadata takes at most ~40% of the budget
-  int64_t Wc = e->chunk_hint > 0 ? e->chunk_hint
-                                  : std::max<int64_t>(kTile, (e->budget * 2 / 5) / per_win);
+  // initial chunk: metadata takes at most ~40% of the budget (the hint of
+  // the last run of the same mode family may be smaller, never larger)
+  const int64_t meta_cap = std::max<int64_t>(kTile, (e->budget * 2 / 5) / per_win / kTile * kTile);
+  int64_t &hint = e->chunk_hint[arena ? 1 : 0];
+  int64_t Wc = hint > 0 ? std::min(hint, meta_cap) : meta_cap;
   Wc = std::min<int64_t>(Wc, round_up(total, kTile));
   Wc = std::max<int64_t>(kTile, Wc / kTile * kTile);
   const double density = (s->P && s->W) ? (double)s->n_toggles / ((double)s->P * s->W) : 0.0;
@@ -660,15 +710,16 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     const int64_t wc = std::min<int64_t>(Wc, w_hi - w);
     const int64_t Wpad = round_up(wc, kTile);
     const int Tc = (int)(Wpad / kTile);
-    TRY(ensure_meta(e, Wpad));
-    if (arena) TRY(ensure_arena(e, Wpad, store));
-    // gate pool: generous estimate of stored toggles, at least 64 MiB
+    // room for the gate pool once this chunk's metadata is allocated: halve
+    // the chunk (before allocating anything) while it does not fit
     const int64_t meta_now = per_win * Wpad;
     int64_t room = e->budget - meta_now - pi_bytes;
     if (room < (int64_t)nregions * 4096) {
       if (Wc > kTile) { Wc = std::max<int64_t>(kTile, Wc / 2 / kTile * kTile); continue; }
       return fail(GS_ERR_CAPACITY, "device memory budget cannot hold one 128-window chunk");
     }
+    TRY(ensure_meta(e, Wpad));
+    if (arena) TRY(ensure_arena(e, Wpad, store));
     const double est_words = (double)G * wc * std::max(2.0, 4.0 * density) * 2.0;
     int64_t want = std::max<int64_t>(pool_bytes, std::max<int64_t>(64ll << 20,
                                      (int64_t)(est_words * sizeof(TS))));
@@ -743,50 +794,28 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     CK(cudaEventRecord(e->ev[1], e->st));
     // ---- K4: per level, one launch per fanin-count group (the launch
     // boundary between levels is the level barrier)
-    // warps the item sizing assumes (GS_ITEM_WARPS: test hook that makes small
-    // designs take the coarse-item and tail-split paths of large ones)
-    static const int64_t item_warps = getenv("GS_ITEM_WARPS") ? atoll(getenv("GS_ITEM_WARPS")) : 0;
-    const int64_t warps = item_warps > 0 ? item_warps : (int64_t)nregions;
-    static const int tail_div = getenv("GS_TAIL_DIV") ? atoi(getenv("GS_TAIL_DIV")) : 2;
-    static const int tail_frac = getenv("GS_TAIL_FRAC") ? atoi(getenv("GS_TAIL_FRAC")) : 2;
-    static const int tail_mult = getenv("GS_TAIL_MULT") ? atoi(getenv("GS_TAIL_MULT")) : 1;
-    static const int item_div = getenv("GS_ITEM_DIV") ? atoi(getenv("GS_ITEM_DIV")) : 4;
-    static const int item_cap = getenv("GS_ITEM_CAP") ? atoi(getenv("GS_ITEM_CAP")) : 12;
     int nl = 0;
+    const int STc = (Tc + kSuper - 1) / kSuper;
     for (int l = 0; l < D->L; ++l) {
       for (int gi = 0; gi < 5; ++gi) {
         const int lo = (int)D->grp[l * 6 + gi];
         const int n = (int)(D->grp[l * 6 + gi + 1] - lo);
         if (n <= 0) continue;
+        const bool lean = narrow && gi < 4;
         LevelArgs A;
         A.lo = lo;
         A.n = n;
-        // items of tpi tiles: enough items for dynamic balance, few enough
-        // that per-item setup and work-counter atomics stay negligible
-        A.tpi = (int)std::max<int64_t>(1, std::min<int64_t>(item_cap, (int64_t)n * Tc / (item_div * warps)));
-        A.tpi = std::min(A.tpi, Tc);
-        while ((int64_t)n * ((Tc + A.tpi - 1) / A.tpi) >= (int64_t(1) << 31)) A.tpi *= 2;
-        A.ntg = (Tc + A.tpi - 1) / A.tpi;
-        // tail: about one head item's worth of tiles per warp, re-cut into
-        // items of tpi / tail_div tiles, so warps finish a launch close
-        // together; only where the column-aligned tail stays within 1 /
-        // tail_frac of the tiles (small items cost per-item setup and L2
-        // reuse).  Defaults from profiles/ab_tail.sh: C2 -3.0 %, C3 -0.7 %.
-        A.tpi2 = std::max(1, A.tpi / tail_div);
-        A.ntg2 = 0;
-        if (tail_div > 1 && A.tpi > 1 && A.ntg > 1) {
-          const int64_t need = std::min<int64_t>((int64_t)(A.ntg - 1) * A.tpi,
-                                                 (tail_mult * warps * A.tpi + n - 1) / n);
-          const int hg = (int)((Tc - need) / A.tpi);  // head groups (whole)
-          if ((int64_t)(Tc - hg * A.tpi) * tail_frac <= Tc) {
-            A.ntg2 = (Tc - hg * A.tpi + A.tpi2 - 1) / A.tpi2;
-            A.ntg = hg;
-          }
-          if ((int64_t)n * (A.ntg + A.ntg2) >= (int64_t(1) << 31)) {
-            A.ntg = (Tc + A.tpi - 1) / A.tpi;
-            A.ntg2 = 0;
-          }
-        }
+        // work items: (gate, run of tiles) for the generic kernel, (gate, run
+        // of 4-tile super-tiles) for the lean kernels, whose CTA is the worker
+        const ItemPlan ip = plan_items(n, lean ? STc : Tc,
+                                       e->item_workers > 0 ? e->item_workers
+                                                           : (lean ? ncta : nregions),
+                                       lean ? kItemCap / kSuper : kItemCap, e->tail_div,
+                                       e->tail_frac);
+        A.tpi = ip.tpi;
+        A.ntg = ip.ntg;
+        A.tpi2 = ip.tpi2;
+        A.ntg2 = ip.ntg2;
         A.pct = pct;
         A.counter = l * 5 + gi;
         const int sm = e->sms;
@@ -870,14 +899,13 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
     // past the metadata share of the budget the first chunk was sized by
     if (used_words > 0) {
       const double fill = (double)used_words / (double)pool_words;
-      const int64_t meta_cap = std::max<int64_t>(kTile, (e->budget * 2 / 5) / per_win / kTile * kTile);
       if (fill < 0.3 && wc == Wc)
         Wc = std::min<int64_t>({round_up(total, kTile), Wc * 2, std::max<int64_t>(Wc, meta_cap)});
     }
     w += wc;
   }
   e->pool_bytes = pool_bytes;
-  e->chunk_hint = Wc;
+  hint = Wc;
   if (store && ro.arena->n_buf)
     CK(cudaMemcpyAsync(ro.arena->buf, e->a_buf, sizeof(long long) * ro.arena->n_buf,
                        cudaMemcpyDeviceToHost, e->st));
@@ -1156,6 +1184,16 @@ int gs_engine_create(gs_design *d, int64_t mem_budget, void *stream, gs_engine *
     return rc;
   }
   *out = e;
+  return GS_OK;
+}
+
+int gs_engine_set_items(gs_engine *e, int64_t workers, int tail_div, int tail_frac) {
+  if (!e) return fail(GS_ERR_ARG, "null engine");
+  if (workers < 0 || tail_div < 1 || tail_frac < 1)
+    return fail(GS_ERR_ARG, "item sizing: workers >= 0, tail_div >= 1, tail_frac >= 1");
+  e->item_workers = workers;
+  e->tail_div = tail_div;
+  e->tail_frac = tail_frac;
   return GS_OK;
 }
 

@@ -6,67 +6,82 @@
 // 0.2 - 0.8 output toggles per gate-window), where most windows of a gate see
 // no input transition at all or exactly one.
 //
-// One warp = one gate x one 128-window tile; lane l owns windows 4l .. 4l+3.
-//   (1) per pin: the tile's count row (one 16-byte load per lane), a warp scan
-//       -> the lane's window offsets in the pin's segment; the pins' segments
-//       are staged into the warp's shared-memory slab by one TMA bulk copy
-//       (cp.async.bulk, completion on an mbarrier) per pin, issued by one lane
-//       and overlapped with the classification below;
-//   (2) classification in registers: windows with no input transition (the
-//       output keeps its window-start value) and with exactly one are
-//       finished by the lane that owns them, in registers -- Algo. 1 with a
-//       single event is one LUT lookup, one delay lookup and one window-end
-//       test (_kernels.py:94-203 with one iteration);
-//   (3) windows with two transitions (worklist, one window per lane): the
-//       closed form of two events, with the interconnect pair filter of a
-//       same-pin pair (_kernels.py:96-117);
-//   (4) windows with three or more (worklist): the lockstep event loop of
-//       sim_span, interconnect filter applied lazily as sim_span does;
-//   (5) compaction: warp scan of the output counts, one pool allocation,
-//       stores straight from registers (windows of (2)) or from the staging
-//       area (windows of (3), (4)); per-net dwell / toggle / filter sums.
+// One CTA = one gate x a super-tile of 4 consecutive 128-window tiles; warp i
+// owns tile i of it and lane l windows 4l .. 4l+3 of that tile.
+//   (A) per warp: per pin the tile's count row (one 16-byte load per lane)
+//       and a warp scan -> the lane's window offsets in the pin's segment;
+//       the pins' segments staged into the warp's shared-memory slab by one
+//       TMA bulk copy (cp.async.bulk, completion on an mbarrier) per pin,
+//       issued by one lane and overlapped with the classification.  Windows
+//       with no input transition (the output keeps its window-start value)
+//       or exactly one are finished by the lane that owns them -- Algo. 1
+//       with a single event is one LUT lookup, one delay lookup and one
+//       window-end test (_kernels.py:94-203, one iteration).  Windows with
+//       more transitions go to the CTA's worklists;
+//   (M) the whole CTA works the pooled lists of its 4 tiles, so the few busy
+//       windows of each tile fill whole warps: two transitions in closed form
+//       (the interconnect pair filter of a same-pin pair, _kernels.py:96-117,
+//       included), three or more through sim_span's event loop with its lazy
+//       interconnect filter;
+//   (C) per warp: warp scan of the output counts, one pool allocation, the
+//       outputs copied out of the staging area; per-net dwell / toggle /
+//       filter sums.
 // Tiles whose fanin toggles do not fit the slab read their segments in place
-// (generic pointers) and stage outputs in the pool; every active window then
-// goes through (3) / (4).
+// (generic pointers) and stage outputs in the pool; all their active windows
+// then go through (M)'s event loop.
 #pragma once
 #include "kernels.cuh"
 
 namespace gs {
 
-// CTAs of 4 warps per SM each fixed-K instance is built for (launch bounds),
-// and the staged words per warp that this occupancy leaves in 228 KB of
-// shared memory (1 KB per CTA reserved)
+// CTAs of 4 warps per SM each fixed-K instance is built for (launch bounds)
 template <int K>
 __host__ __device__ constexpr int lean_ctas() { return K <= 2 ? 8 : K == 3 ? 7 : 6; }
 
-template <int K>
-struct LeanFixed {
-  unsigned offs[K][kTile + 4];
-  unsigned cnt[kTile];
-  unsigned list[kTile];
-  unsigned arcs[K * (1 << (K - 1)) * 2];
-  unsigned dtab[K <= 2 ? (1 << (2 * K)) * 2 : K * (1 << K) * 2];
-  unsigned long long mbar;
-  unsigned next;
+constexpr int kSuper = kEvalWarps;         // tiles per CTA step (one per warp)
+constexpr int kPool = kSuper * kTile;      // windows per CTA step
+
+// per-warp part: staged segments and tile state
+template <int K, int SLAB>
+struct alignas(16) LeanWarp {
+  unsigned slab[SLAB];                       // staged fanin segments, then outputs
+  alignas(16) unsigned offs[K][kTile + 4];   // pin p: window w's toggles start at offs[p][w]
+  alignas(16) unsigned cnt[kTile];           // stored toggles per window
+  unsigned long long tb[K];                  // in place: pin p's tile base in `data`
+  unsigned long long stage;                  // generic address of the output staging area
+  unsigned seg[K];                           // staged: pin p's segment at slab[seg[p]]
+  int t;                                     // tile index
+  int in_smem;
+  unsigned long long mbar;                   // bulk-copy completion
 };
 
 template <int K>
+struct LeanShared {
+  unsigned short list[2][kPool];             // worklists of a step: [0] loop, [1] two
+  unsigned arcs[K * (1 << (K - 1)) * 2];
+  unsigned dtab[K <= 2 ? (1 << (2 * K)) * 2 : K * (1 << K) * 2];
+  unsigned nlist[2][2];                      // list lengths, double-buffered by step parity
+  unsigned item;
+};
+
+// staged words per warp that the occupancy leaves in 228 KB of shared memory
+// (1 KB per CTA reserved)
+template <int K>
 __host__ __device__ constexpr int lean_slab_words() {
-  return (int)((((233472 / lean_ctas<K>() - 1024) / kEvalWarps) - sizeof(LeanFixed<K>) - 16) / 16 * 4);
+  return (int)(((233472 / lean_ctas<K>() - 1024 - sizeof(LeanShared<K>) - 64) / kEvalWarps -
+                sizeof(LeanWarp<K, 4>) + 16) / 16 * 4);
 }
 
 template <int K>
 struct alignas(16) LeanSmem {
-  unsigned slab[lean_slab_words<K>()];       // staged fanin segments, then multi-window outputs
-  alignas(16) unsigned offs[K][kTile + 4];   // pin p: window w's toggles start at offs[p][w]
-  alignas(16) unsigned cnt[kTile];           // stored toggles of the worklist windows
-  unsigned list[kTile];                      // worklist: w | start input vector << 8
-  // the item's condition tables and the delay table built from them
-  unsigned arcs[K * (1 << (K - 1)) * 2];
-  unsigned dtab[K <= 2 ? (1 << (2 * K)) * 2 : K * (1 << K) * 2];
-  unsigned long long mbar;                   // bulk-copy completion
-  unsigned next;                             // dynamic worklist counter (event loop)
+  LeanWarp<K, lean_slab_words<K>()> w[kEvalWarps];
+  LeanShared<K> s;
 };
+
+template <int K>
+constexpr size_t lean_smem_bytes() {
+  return sizeof(LeanSmem<K>);
+}
 
 // ---------------------------------------------------------------- TMA bulk
 __device__ __forceinline__ unsigned smem_addr(const void *p) {
@@ -121,451 +136,11 @@ struct LeanAcc {
   int disc = 0;
 };
 
-// ------------------------------------------------------- (4) event loop
-// sim_span's event loop (_kernels.py:94-203) for the worklist windows with
-// three or more input transitions; a lane whose window is finished takes the
-// next one from the shared counter.  Inputs come from `src` (staged or in
-// place); the interconnect pair filter runs lazily exactly as sim_span's
-// refresh (_kernels.py:96-117).
-template <int MODE, int K, bool PCT100>
-__device__ __forceinline__ void lean_loop(const ChunkDev &C, int g, unsigned long long lut,
-                                          const unsigned (&ic)[K], int pct, LeanSmem<K> &S,
-                                          const unsigned *const (&src)[K], unsigned *stage,
-                                          int base_w, unsigned nwork, LeanAcc &acc) {
-  constexpr unsigned INF = 0xffffffffu;
-  unsigned cur[K], end[K], nxt[K];
-  unsigned idx = 0, y = 0, y0 = 0, so = 0, wlen = 0, t_last = 0, t_stored = 0, dt = 0, t1w = 0,
-           dv = 0;
-  int w = -1, cnt = 0, peak = 0, filt = 0, icf = 0, disc = 0;
-  bool has = false, has_last = false, last_stored = false;
-  auto refresh = [&](int p) {
-    unsigned q = cur[p];
-    const unsigned d = ic[p];
-    if (d > 0) {
-      while (q + 1 < end[p] && src[p][q + 1] - src[p][q] < d) {
-        q += 2;
-        ++icf;
-      }
-      cur[p] = q;
-    }
-    nxt[p] = q < end[p] ? src[p][q] + d : INF;
-  };
-  auto start = [&](unsigned i) {
-    const unsigned e = S.list[i];
-    w = (int)(e & 0xFFu);
-    idx = e >> 8;
-    has = true;
-    cnt = peak = filt = icf = disc = 0;
-    so = 0;
-#pragma unroll
-    for (int p = 0; p < K; ++p) {
-      cur[p] = S.offs[p][w];
-      end[p] = S.offs[p][w + 1];
-      so += cur[p];
-      refresh(p);
-    }
-    y0 = y = (unsigned)(lut >> idx) & 1u;
-    wlen = __ldg(C.wlen32 + base_w + w);
-    has_last = last_stored = false;
-    dv = y0;
-    dt = t1w = 0;
-  };
-  auto finish = [&]() {
-    if (has_last && last_stored) {
-      stage[so + cnt] = t_last;
-      ++cnt;
-      peak = max(peak, cnt);
-      t1w += dv ? t_last - dt : 0u;
-      dv ^= 1u;
-      dt = t_last;
-    }
-    if (PCT100) {
-      acc.t1 += (long long)(t1w + (dv ? wlen - dt : 0u));
-    } else {
-      // below 100 % stored edges may be popped: the dwell comes from the
-      // final stored waveform (dwell_sweep, _kernels.py:254-295)
-      unsigned v = y0, prev = 0;
-      long long a1 = 0;
-      for (int q = 0; q < cnt; ++q) {
-        const unsigned x = stage[so + q];
-        if (v) a1 += x - prev;
-        v ^= 1u;
-        prev = x;
-      }
-      if (v) a1 += wlen - prev;
-      acc.t1 += a1;
-    }
-    S.cnt[w] = (unsigned)cnt;
-    acc.filt += (unsigned)filt;
-    acc.icf += (unsigned)icf;
-    acc.disc += disc;
-    record_arena<MODE, unsigned>(C, g, base_w + w, cnt, peak, filt, icf, disc, y0,
-                                 [&](int j) -> unsigned & { return stage[so + j]; });
-    has = false;
-  };
-  auto first_event = [&]() {
-    unsigned t = nxt[0];
-#pragma unroll
-    for (int p = 1; p < K; ++p) t = min(t, nxt[p]);
-    return t;
-  };
-  volatile unsigned *next = &S.next;
-  unsigned tmin = INF;
-  auto refill = [&]() {
-    while (*next < nwork) {
-      if (has) finish();
-      const unsigned nw = atomicAdd(&S.next, 1u);
-      if (nw >= nwork) break;
-      start(nw);
-      tmin = first_event();
-      if (tmin != INF) break;
-    }
-  };
-  if (lane_id() < nwork) {
-    start(lane_id());
-    tmin = first_event();
-    if (tmin == INF) refill();
-  }
-  while (true) {
-    const bool live = has && tmin != INF;
-    if (!__any_sync(0xffffffffu, live)) break;
-    if (live) {
-      unsigned sw = 0;
-#pragma unroll
-      for (int p = 0; p < K; ++p) sw |= (nxt[p] == tmin ? 1u : 0u) << p;
-      idx ^= sw;
-#pragma unroll
-      for (int p = 0; p < K; ++p)
-        if ((sw >> p) & 1u) {
-          cur[p] += 1;
-          refresh(p);
-        }
-      // output side (K:136-193), as selects so the lanes stay converged
-      const unsigned ny = (unsigned)(lut >> idx) & 1u;
-      const bool chg = ny != y;
-      const int col = ny ? 0 : 1;
-      const unsigned dly = dtab_delay<K>(S.dtab, sw, idx, col);
-      const unsigned t_out = tmin + dly;
-      const unsigned thr = PCT100 ? dly : (unsigned)((unsigned long long)dly * (unsigned)pct / 100u);
-      bool cancel;
-      if constexpr (PCT100) {
-        // only the pending edge can be cancelled at 100 %: stored edges are final
-        cancel = chg && has_last && (t_out <= t_last || t_out - t_last < thr);
-      } else {
-        const bool have = has_last || cnt > 0;
-        const unsigned tgt = has_last ? t_last : t_stored;
-        cancel = chg && have && (t_out <= tgt || t_out - tgt < thr);
-      }
-      const bool emit = chg && !cancel;
-      const bool pop = !PCT100 && cancel && !has_last;
-      disc -= (cancel && has_last && !last_stored) ? 1 : 0;
-      if (!PCT100) {
-        cnt -= pop ? 1 : 0;
-        if (pop && cnt > 0) t_stored = stage[so + cnt - 1];
-      }
-      filt += cancel ? 1 : 0;
-      const bool store = emit && has_last && last_stored;
-      if (store) stage[so + cnt] = t_last;
-      if (!PCT100) t_stored = store ? t_last : t_stored;
-      cnt += store ? 1 : 0;
-      if (MODE != MODE_STATS) peak = max(peak, cnt);
-      t1w += (store && dv) ? t_last - dt : 0u;
-      dv ^= store ? 1u : 0u;
-      dt = store ? t_last : dt;
-      const bool inwin = t_out < wlen;
-      disc += (emit && !inwin) ? 1 : 0;
-      last_stored = emit ? inwin : last_stored;
-      t_last = emit ? t_out : t_last;
-      has_last = emit || (has_last && !cancel);
-      y = chg ? ny : y;
-      tmin = first_event();
-      if (tmin == INF) refill();
-    }
-  }
-  if (has) finish();
-}
-
-// ------------------------------------------------------------ one tile
-// Per-lane window metadata, 8 bits per window j of the lane: start input
-// vector (bits 0-3), the pin of a single transition (4-5), class (6-7).
-enum LeanClass : unsigned { CL_QUIET = 0, CL_ONE = 1, CL_TWO = 2, CL_LOOP = 3 };
-__device__ __forceinline__ unsigned meta_ix(unsigned m, int j) { return (m >> (8 * j)) & 15u; }
-__device__ __forceinline__ unsigned meta_pin(unsigned m, int j) { return (m >> (8 * j + 4)) & 3u; }
-__device__ __forceinline__ unsigned meta_cls(unsigned m, int j) { return (m >> (8 * j + 6)) & 3u; }
-
-template <int MODE, int K, bool PCT100>
-__device__ __forceinline__ void lean_tile(const ChunkDev &C, int g, int gnet,
-                                          unsigned long long lut, const int (&net)[K],
-                                          const unsigned (&ic)[K], int t, int pct, LeanSmem<K> &S,
-                                          Region &R, unsigned &phase, LeanAcc &acc) {
-  constexpr int SLAB = lean_slab_words<K>();
-  const unsigned lane = lane_id();
-  const int base_w = t * kTile;
-  const int nact = min(kTile, C.Wc - base_w);
-  const int wl = (int)lane * kWPL;
-  const int Tw = C.Wpad / 32;
-  unsigned *data = reinterpret_cast<unsigned *>(C.data);
-
-  GS_PROF_T(pt0);
-  GS_PROF_ADD(PF_TILES, 1);
-  // ---- (1) fanin count rows -> window offsets; staging plan
-  unsigned c[K][kWPL];
-  unsigned long long tb[K];
-  unsigned bits[K];
-#pragma unroll
-  for (int p = 0; p < K; ++p) {
-    load_counts(C.cnt + (size_t)net[p] * C.Wpad + base_w + wl, c[p]);
-    tb[p] = __ldg(C.tbase + (size_t)net[p] * C.Tc + t);
-    bits[p] = load_init_bits(C.init + (size_t)net[p] * Tw, t);
-  }
-  unsigned n[kWPL], sidx[kWPL], meta = 0;
-#pragma unroll
-  for (int j = 0; j < kWPL; ++j) n[j] = sidx[j] = 0;
-  unsigned tot[K], seg[K], inw = 0, UB = 0;
-#pragma unroll
-  for (int p = 0; p < K; ++p) {
-    unsigned s4 = 0;
-#pragma unroll
-    for (int j = 0; j < kWPL; ++j) s4 += c[p][j];
-    unsigned ex = warp_excl_scan(s4, &tot[p]);
-    const unsigned sh = (unsigned)tb[p] & 3u;
-    seg[p] = inw + sh;
-    inw += tot[p] ? (sh + tot[p] + 3u) & ~3u : 0u;
-    UB += tot[p];
-    unsigned o4[kWPL];
-#pragma unroll
-    for (int j = 0; j < kWPL; ++j) {
-      o4[j] = ex;
-      // the single transition of a one-transition window: its slab position
-      if (c[p][j]) {
-        sidx[j] = seg[p] + ex;
-        meta = (meta & ~(3u << (8 * j + 4))) | ((unsigned)p << (8 * j + 4));
-      }
-      n[j] += c[p][j];
-      meta |= ((bits[p] >> j) & 1u) << (8 * j + p);
-      ex += c[p][j];
-    }
-    st4(&S.offs[p][wl], o4);
-    if (lane == kWarp - 1) S.offs[p][kTile] = tot[p];
-  }
-  // inputs (aligned per pin) and worklist outputs (UB words) in the slab, or
-  // both in global memory
-  const bool in_smem = inw + UB <= (unsigned)SLAB;
-  const unsigned *src[K];
-  unsigned *stage;
-  bool ok = true;
-  if (in_smem) {
-    if (inw) {
-      __syncwarp();
-      if (lane == 0) {
-        fence_proxy_async();  // the slab's previous generic accesses before the async writes
-        mbar_expect_tx(&S.mbar, inw * 4u);
-#pragma unroll
-        for (int p = 0; p < K; ++p)
-          if (tot[p]) {
-            const unsigned sh = (unsigned)tb[p] & 3u;
-            bulk_g2s(&S.slab[seg[p] - sh], data + (tb[p] - sh), ((sh + tot[p] + 3u) & ~3u) * 4u,
-                     &S.mbar);
-          }
-      }
-    }
-#pragma unroll
-    for (int p = 0; p < K; ++p) src[p] = &S.slab[seg[p]];
-    stage = &S.slab[inw];
-  } else {
-#pragma unroll
-    for (int p = 0; p < K; ++p) src[p] = data + tb[p];
-    const unsigned long long sb = region_alloc(C, R, UB);
-    ok = sb != ~0ull;
-    stage = data + (ok ? sb : 0ull);
-  }
-
-  // ---- (2) classes; worklist of the windows with >= 2 transitions (>= 1
-  // when reading in place), loop windows (>= 3) at the front.  A single
-  // transition's slab position waits in S.cnt until the inline pass.
-  unsigned cl = 0;
-#pragma unroll
-  for (int j = 0; j < kWPL; ++j) {
-    const bool act = ok && wl + j < nact;
-    const unsigned k = !act || n[j] == 0 ? CL_QUIET
-                       : !in_smem || n[j] > 2 ? CL_LOOP
-                       : n[j] == 2 ? CL_TWO : CL_ONE;
-    meta |= k << (8 * j + 6);
-    cl += k == CL_LOOP ? 1u : k == CL_TWO ? 1u << 16 : 0u;
-  }
-  st4(&S.cnt[wl], sidx);
-  unsigned tot2;
-  {
-    const unsigned x = warp_excl_scan(cl, &tot2);
-    unsigned xl = x & 0xFFFFu, xt = (tot2 & 0xFFFFu) + (x >> 16);
-#pragma unroll
-    for (int j = 0; j < kWPL; ++j) {
-      const unsigned k = meta_cls(meta, j);
-      if (k >= CL_TWO) S.list[k == CL_LOOP ? xl++ : xt++] = (unsigned)(wl + j) | (meta_ix(meta, j) << 8);
-    }
-  }
-  if (lane == 0) S.next = kWarp;
-  // wait for the staged segments (all lanes observe the barrier phase)
-  if (in_smem && inw) {
-    mbar_wait(&S.mbar, phase);
-    phase ^= 1u;
-  }
-  __syncwarp();
-  GS_PROF_T(pt1);
-  GS_PROF_ADD(PF_PHASE1, pt1 - pt0);
-
-  // ---- (3) two transitions, closed form (one window per lane per round).
-  // With no edge pending at the first event, Algo. 1's output side
-  // (K:136-203) collapses to selects: event 1 (both pins when the two
-  // transitions coincide) can only emit; event 2 can emit, cancel event 1's
-  // edge, or leave it pending; no stored edge can be popped.
-  const unsigned nloop = tot2 & 0xFFFFu, nlist = nloop + (tot2 >> 16);
-  for (unsigned i = nloop + lane; i < nlist; i += kWarp) {
-    const unsigned e = S.list[i];
-    const int w = (int)(e & 0xFFu);
-    const unsigned i0 = e >> 8;
-    unsigned nt = 0, pa = 0, pb = 0, so = 0;
-    const unsigned *qa = src[0], *qb = src[0];
-#pragma unroll
-    for (int p = 0; p < K; ++p) {
-      const unsigned a = S.offs[p][w], m = S.offs[p][w + 1] - a;
-      so += a;
-      pa = (m >= 1 && nt == 0) ? (unsigned)p : pa;
-      qa = (m >= 1 && nt == 0) ? src[p] + a : qa;
-      pb = ((m >= 1 && nt == 1) || (m >= 2 && nt == 0)) ? (unsigned)p : pb;
-      qb = (m >= 1 && nt == 1) ? src[p] + a : (m >= 2 && nt == 0) ? src[p] + a + 1 : qb;
-      nt += m;
-    }
-    unsigned ica = ic[0], icb = ic[0];
-#pragma unroll
-    for (int p = 1; p < K; ++p) {
-      ica = pa == (unsigned)p ? ic[p] : ica;
-      icb = pb == (unsigned)p ? ic[p] : icb;
-    }
-    const unsigned va = *qa, vb = *qb;
-    // a same-pin pair narrower than the pin's interconnect delay is
-    // filtered out whole (_kernels.py:96-117): no event remains
-    const bool pairf = pa == pb && ica > 0 && vb - va < ica;
-    unsigned ta = va + ica, tb2 = vb + icb;
-    const bool sw2 = tb2 < ta;
-    { const unsigned tt = sw2 ? tb2 : ta; tb2 = sw2 ? ta : tb2; ta = tt; }
-    { const unsigned pp = sw2 ? pb : pa; pb = sw2 ? pa : pb; pa = pp; }
-    const bool both = ta == tb2 && pa != pb;  // two pins at one instant: one event
-    const bool n1 = !pairf, n2 = !pairf && !both;
-    const unsigned s1 = (1u << pa) | (both ? (1u << pb) : 0u), s2 = 1u << pb;
-    const unsigned i1 = i0 ^ (n1 ? s1 : 0u), i2 = i1 ^ (n2 ? s2 : 0u);
-    const unsigned yy0 = (unsigned)(lut >> i0) & 1u;
-    const unsigned y1 = (unsigned)(lut >> i1) & 1u;
-    const unsigned y2 = (unsigned)(lut >> i2) & 1u;
-    const bool c1 = y1 != yy0, c2 = y2 != y1;
-    const unsigned d2 = dtab_delay<K>(S.dtab, s2, i2, y2 ? 0 : 1);
-    const unsigned o1 = ta + dtab_delay<K>(S.dtab, s1, i1, y1 ? 0 : 1);
-    const unsigned o2 = tb2 + d2;
-    const unsigned thr = PCT100 ? d2 : (unsigned)((unsigned long long)d2 * (unsigned)pct / 100u);
-    const unsigned wlw = __ldg(C.wlen32 + base_w + w);
-    const bool x2 = c2 && c1 && (o2 <= o1 || o2 - o1 < thr);   // edge 1 cancelled
-    const bool e2 = c2 && !x2;                                 // edge 2 emitted
-    const bool in1 = o1 < wlw, in2 = o2 < wlw;
-    const bool st1 = e2 && c1 && in1;                          // edge 1 stored at event 2
-    const unsigned tp = e2 ? o2 : o1;                          // pending at the end
-    const bool fl = e2 ? in2 : (c1 && !x2 && in1);             // ... and flushed
-    const unsigned cnt = (st1 ? 1u : 0u) + (fl ? 1u : 0u);
-    const unsigned f0 = st1 ? o1 : tp;
-    unsigned *st = stage + so;
-    if (cnt >= 1) st[0] = f0;
-    if (cnt == 2) st[1] = tp;
-    const int disc = (c1 && !in1 ? 1 : 0) + (e2 && !in2 ? 1 : 0) - (x2 && !in1 ? 1 : 0);
-    // dwell at 1: +-edge times by the value before each edge, plus the
-    // window end when the final value is 1 (wrapping arithmetic, exact
-    // since the result lies in [0, wlen])
-    const unsigned e0 = cnt >= 1 ? f0 : 0u, e1 = cnt == 2 ? tp : 0u;
-    const unsigned wf = (cnt & 1u) ? (yy0 ? 0u : wlw) : (yy0 ? wlw : 0u);
-    acc.t1 += (long long)(yy0 ? e0 - e1 + wf : e1 - e0 + wf);
-    S.cnt[w] = cnt;
-    acc.filt += x2 ? 1u : 0u;
-    acc.icf += pairf ? 1u : 0u;
-    acc.disc += disc;
-    if (MODE != MODE_STATS)
-      record_arena<MODE, unsigned>(C, g, base_w + w, (int)cnt, (int)cnt, x2 ? 1 : 0,
-                                   pairf ? 1 : 0, disc, yy0,
-                                   [&](int q) -> unsigned & { return st[q]; });
-  }
-  GS_PROF_T(pt2);
-  GS_PROF_ADD(PF_CLOSED, pt2 - pt1);
-  GS_PROF_ADD(PF_LOOP_WINDOWS, nloop);
-  GS_PROF_ADD(PF_TRIVIAL, nlist - nloop);
-  // ---- (4) three or more transitions: the event loop
-  if (nloop) lean_loop<MODE, K, PCT100>(C, g, lut, ic, pct, S, src, stage, base_w, nloop, acc);
-  __syncwarp();
-  GS_PROF_T(pt3);
-  GS_PROF_ADD(PF_LOOP, pt3 - pt2);
-
-  // ---- (5) the lane's own windows: quiet and single-transition windows in
-  // registers, then compaction and the per-net sums
-  unsigned cm[kWPL], wlen[kWPL], ot[kWPL], co[kWPL], nib = 0, s = 0;
-  ld4(&S.cnt[wl], cm);   // worklist windows: stored count; one-transition: slab position
-  load_counts(C.wlen32 + base_w + wl, wlen);
-#pragma unroll
-  for (int j = 0; j < kWPL; ++j) {
-    const unsigned k = meta_cls(meta, j), ix = meta_ix(meta, j), p1 = meta_pin(meta, j);
-    const bool act = ok && wl + j < nact;
-    const bool one = k == CL_ONE;
-    unsigned icp = ic[0];
-#pragma unroll
-    for (int p = 1; p < K; ++p) icp = p1 == (unsigned)p ? ic[p] : icp;
-    const unsigned tv = one ? S.slab[one ? cm[j] : 0u] + icp : 0u;
-    const unsigned y0 = (unsigned)(lut >> ix) & 1u;
-    const unsigned i1 = ix ^ (1u << p1);
-    const unsigned y1 = (unsigned)(lut >> i1) & 1u;
-    const bool chg = one && y1 != y0;
-    ot[j] = tv + dtab_pin<K>(S.dtab, p1, i1, y1 ? 0u : 1u);
-    const bool inwin = ot[j] < wlen[j];
-    const bool st = chg && inwin;
-    const bool inl = act && k <= CL_ONE;
-    acc.disc += (chg && !inwin) ? 1 : 0;
-    acc.t1 += inl ? (y0 ? (st ? ot[j] : wlen[j]) : (st ? wlen[j] - ot[j] : 0u)) : 0u;
-    co[j] = !act ? 0u : k >= CL_TWO ? cm[j] : st ? 1u : 0u;
-    nib |= (act ? y0 : 0u) << j;
-    s += co[j];
-    if (MODE != MODE_STATS && inl)
-      record_arena<MODE, unsigned>(C, g, base_w + wl + j, (int)co[j], (int)co[j], 0, 0,
-                                   (chg && !inwin) ? 1 : 0, y0,
-                                   [&](int) -> unsigned & { return ot[j]; });
-  }
-  unsigned CNT;
-  const unsigned cx = warp_excl_scan(s, &CNT);
-  const unsigned long long ob = CNT ? region_alloc(C, R, CNT) : 0ull;
-  const bool wrote = ob != ~0ull;  // else the chunk is re-run; keep readers in bounds
-  if (wrote) {
-    unsigned *dst = data + ob + cx;
-#pragma unroll
-    for (int j = 0; j < kWPL; ++j) {
-      if (meta_cls(meta, j) <= CL_ONE) {
-        if (co[j]) dst[0] = ot[j];
-      } else if (co[j]) {
-        unsigned so = 0;
-#pragma unroll
-        for (int p = 0; p < K; ++p) so += S.offs[p][wl + j];
-        for (unsigned q = 0; q < co[j]; ++q) dst[q] = stage[so + q];
-      }
-      dst += co[j];
-    }
-  }
-  acc.tc += s;
-  // the gate's own net: tile base, counts, window-start bits
-  if (lane == 0) C.tbase[(size_t)gnet * C.Tc + t] = wrote ? ob : 0ull;
-  store_counts(C.cnt + (size_t)gnet * C.Wpad + base_w + wl, co, wrote);
-  store_init_words(C.init + (size_t)gnet * Tw, t, nib);
-  __syncwarp();
-  GS_PROF_T(pt4);
-  GS_PROF_ADD(PF_PHASE3, pt4 - pt3);
-}
-
 // condition tables of one gate -> smem: arcs[(p << (K-1) | row) * 2 + col],
 // then the delay table of the event step: k <= 2 by (switching pin set,
 // post-transition inputs, edge) -- the max over the switching arcs of the
 // conditioned delay (K:139-151); k = 3, 4 by (single pin, inputs, edge),
-// simultaneous pins taking the max of their entries
+// simultaneous pins taking the max of their entries.  One warp builds it.
 template <int K>
 __device__ __forceinline__ void build_dtab(unsigned *arcs, unsigned *dtab,
                                            const unsigned *__restrict__ arc32,
@@ -598,40 +173,270 @@ __device__ __forceinline__ void build_dtab(unsigned *arcs, unsigned *dtab,
       dtab[i] = arcs[((pp * R) + row_of(id, pp)) * 2 + col];
     }
   }
-  __syncwarp();
 }
 
+// ---------------------------------------------------- worklist windows
+// A worklist entry: window (7 bits) | start input vector (4) | warp (2).
+__device__ __forceinline__ unsigned short wl_entry(int w, unsigned ix, int warp) {
+  return (unsigned short)((unsigned)w | (ix << 7) | ((unsigned)warp << 11));
+}
+
+// the staged-or-in-place sources of warp `wi`'s tile
+template <int K, int SLAB>
+__device__ __forceinline__ void tile_sources(const ChunkDev &C, LeanWarp<K, SLAB> &T,
+                                             const unsigned *(&src)[K]) {
+  unsigned *data = reinterpret_cast<unsigned *>(C.data);
+#pragma unroll
+  for (int p = 0; p < K; ++p) src[p] = T.in_smem ? &T.slab[T.seg[p]] : data + T.tb[p];
+}
+
+// sim_span's event loop (_kernels.py:94-203) over one window with three or
+// more input transitions, the interconnect pair filter applied lazily as
+// sim_span's refresh does (_kernels.py:96-117).  Outputs go to the tile's
+// staging area at the window's slot.
+template <int MODE, int K, bool PCT100, int SLAB>
+__device__ __forceinline__ void loop_window(const ChunkDev &C, int g, unsigned long long lut,
+                                            const unsigned (&ic)[K], int pct,
+                                            const unsigned *dtab, LeanWarp<K, SLAB> &T, int w,
+                                            unsigned idx, LeanAcc &acc) {
+  constexpr unsigned INF = 0xffffffffu;
+  const unsigned *src[K];
+  tile_sources<K, SLAB>(C, T, src);
+  unsigned *stage = reinterpret_cast<unsigned *>(T.stage);
+  const int base_w = T.t * kTile;
+  unsigned cur[K], end[K], nxt[K], so = 0;
+  int icf = 0;
+  auto refresh = [&](int p) {
+    unsigned q = cur[p];
+    const unsigned d = ic[p];
+    if (d > 0) {
+      while (q + 1 < end[p] && src[p][q + 1] - src[p][q] < d) {
+        q += 2;
+        ++icf;
+      }
+      cur[p] = q;
+    }
+    nxt[p] = q < end[p] ? src[p][q] + d : INF;
+  };
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    cur[p] = T.offs[p][w];
+    end[p] = T.offs[p][w + 1];
+    so += cur[p];
+    refresh(p);
+  }
+  const unsigned y0 = (unsigned)(lut >> idx) & 1u;
+  const unsigned wlen = __ldg(C.wlen32 + base_w + w);
+  unsigned y = y0, t_last = 0, t_stored = 0, dt = 0, t1w = 0, dv = y0;
+  int cnt = 0, peak = 0, filt = 0, disc = 0;
+  bool has_last = false, last_stored = false;
+  while (true) {
+    unsigned tmin = nxt[0];
+#pragma unroll
+    for (int p = 1; p < K; ++p) tmin = min(tmin, nxt[p]);
+    if (tmin == INF) break;
+    // every pin arriving at tmin switches (MSI), then advances
+    unsigned sw = 0;
+#pragma unroll
+    for (int p = 0; p < K; ++p) sw |= (nxt[p] == tmin ? 1u : 0u) << p;
+    idx ^= sw;
+#pragma unroll
+    for (int p = 0; p < K; ++p)
+      if ((sw >> p) & 1u) {
+        cur[p] += 1;
+        refresh(p);
+      }
+    // output side (K:136-193)
+    const unsigned ny = (unsigned)(lut >> idx) & 1u;
+    const bool chg = ny != y;
+    const unsigned dly = dtab_delay<K>(dtab, sw, idx, ny ? 0 : 1);
+    const unsigned t_out = tmin + dly;
+    const unsigned thr = PCT100 ? dly : (unsigned)((unsigned long long)dly * (unsigned)pct / 100u);
+    bool cancel;
+    if constexpr (PCT100) {
+      // only the pending edge can be cancelled at 100 %: stored edges are final
+      cancel = chg && has_last && (t_out <= t_last || t_out - t_last < thr);
+    } else {
+      const bool have = has_last || cnt > 0;
+      const unsigned tgt = has_last ? t_last : t_stored;
+      cancel = chg && have && (t_out <= tgt || t_out - tgt < thr);
+    }
+    const bool emit = chg && !cancel;
+    const bool pop = !PCT100 && cancel && !has_last;
+    disc -= (cancel && has_last && !last_stored) ? 1 : 0;
+    if (!PCT100) {
+      cnt -= pop ? 1 : 0;
+      if (pop && cnt > 0) t_stored = stage[so + cnt - 1];
+    }
+    filt += cancel ? 1 : 0;
+    const bool store = emit && has_last && last_stored;
+    if (store) stage[so + cnt] = t_last;
+    if (!PCT100) t_stored = store ? t_last : t_stored;
+    cnt += store ? 1 : 0;
+    if (MODE != MODE_STATS) peak = max(peak, cnt);
+    t1w += (store && dv) ? t_last - dt : 0u;
+    dv ^= store ? 1u : 0u;
+    dt = store ? t_last : dt;
+    const bool inwin = t_out < wlen;
+    disc += (emit && !inwin) ? 1 : 0;
+    last_stored = emit ? inwin : last_stored;
+    t_last = emit ? t_out : t_last;
+    has_last = emit || (has_last && !cancel);
+    y = chg ? ny : y;
+  }
+  if (has_last && last_stored) {
+    stage[so + cnt] = t_last;
+    ++cnt;
+    peak = max(peak, cnt);
+    t1w += dv ? t_last - dt : 0u;
+    dv ^= 1u;
+    dt = t_last;
+  }
+  if (PCT100) {
+    acc.t1 += (long long)(t1w + (dv ? wlen - dt : 0u));
+  } else {
+    // below 100 % stored edges may be popped: the dwell comes from the final
+    // stored waveform (dwell_sweep, _kernels.py:254-295)
+    unsigned v = y0, prev = 0;
+    long long a1 = 0;
+    for (int q = 0; q < cnt; ++q) {
+      const unsigned x = stage[so + q];
+      if (v) a1 += x - prev;
+      v ^= 1u;
+      prev = x;
+    }
+    if (v) a1 += wlen - prev;
+    acc.t1 += a1;
+  }
+  T.cnt[w] = (unsigned)cnt;
+  acc.filt += (unsigned)filt;
+  acc.icf += (unsigned)icf;
+  acc.disc += disc;
+  record_arena<MODE, unsigned>(C, g, base_w + w, cnt, peak, filt, icf, disc, y0,
+                               [&](int j) -> unsigned & { return stage[so + j]; });
+}
+
+// Two input transitions in closed form.  With no edge pending at the first
+// event, Algo. 1's output side (K:136-203) collapses to selects: event 1 (both
+// pins when the two transitions coincide) can only emit; event 2 can emit,
+// cancel event 1's edge, or leave it pending; no stored edge can be popped.
+template <int MODE, int K, bool PCT100, int SLAB>
+__device__ __forceinline__ void two_window(const ChunkDev &C, int g, unsigned long long lut,
+                                           const unsigned (&ic)[K], int pct,
+                                           const unsigned *dtab, LeanWarp<K, SLAB> &T, int w,
+                                           unsigned i0, LeanAcc &acc) {
+  const unsigned *src[K];
+  tile_sources<K, SLAB>(C, T, src);
+  unsigned *stage = reinterpret_cast<unsigned *>(T.stage);
+  const int base_w = T.t * kTile;
+  unsigned nt = 0, pa = 0, pb = 0, so = 0;
+  const unsigned *qa = src[0], *qb = src[0];
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    const unsigned a = T.offs[p][w], m = T.offs[p][w + 1] - a;
+    so += a;
+    pa = (m >= 1 && nt == 0) ? (unsigned)p : pa;
+    qa = (m >= 1 && nt == 0) ? src[p] + a : qa;
+    pb = ((m >= 1 && nt == 1) || (m >= 2 && nt == 0)) ? (unsigned)p : pb;
+    qb = (m >= 1 && nt == 1) ? src[p] + a : (m >= 2 && nt == 0) ? src[p] + a + 1 : qb;
+    nt += m;
+  }
+  unsigned ica = ic[0], icb = ic[0];
+#pragma unroll
+  for (int p = 1; p < K; ++p) {
+    ica = pa == (unsigned)p ? ic[p] : ica;
+    icb = pb == (unsigned)p ? ic[p] : icb;
+  }
+  const unsigned va = *qa, vb = *qb;
+  // a same-pin pair narrower than the pin's interconnect delay is filtered
+  // out whole (_kernels.py:96-117): no event remains
+  const bool pairf = pa == pb && ica > 0 && vb - va < ica;
+  unsigned ta = va + ica, tb2 = vb + icb;
+  const bool sw2 = tb2 < ta;
+  { const unsigned tt = sw2 ? tb2 : ta; tb2 = sw2 ? ta : tb2; ta = tt; }
+  { const unsigned pp = sw2 ? pb : pa; pb = sw2 ? pa : pb; pa = pp; }
+  const bool both = ta == tb2 && pa != pb;  // two pins at one instant: one event
+  const bool n1 = !pairf, n2 = !pairf && !both;
+  const unsigned s1 = (1u << pa) | (both ? (1u << pb) : 0u), s2 = 1u << pb;
+  const unsigned i1 = i0 ^ (n1 ? s1 : 0u), i2 = i1 ^ (n2 ? s2 : 0u);
+  const unsigned yy0 = (unsigned)(lut >> i0) & 1u;
+  const unsigned y1 = (unsigned)(lut >> i1) & 1u;
+  const unsigned y2 = (unsigned)(lut >> i2) & 1u;
+  const bool c1 = y1 != yy0, c2 = y2 != y1;
+  const unsigned d2 = dtab_delay<K>(dtab, s2, i2, y2 ? 0 : 1);
+  const unsigned o1 = ta + dtab_delay<K>(dtab, s1, i1, y1 ? 0 : 1);
+  const unsigned o2 = tb2 + d2;
+  const unsigned thr = PCT100 ? d2 : (unsigned)((unsigned long long)d2 * (unsigned)pct / 100u);
+  const unsigned wlw = __ldg(C.wlen32 + base_w + w);
+  const bool x2 = c2 && c1 && (o2 <= o1 || o2 - o1 < thr);   // edge 1 cancelled
+  const bool e2 = c2 && !x2;                                 // edge 2 emitted
+  const bool in1 = o1 < wlw, in2 = o2 < wlw;
+  const bool st1 = e2 && c1 && in1;                          // edge 1 stored at event 2
+  const unsigned tp = e2 ? o2 : o1;                          // pending at the end
+  const bool fl = e2 ? in2 : (c1 && !x2 && in1);             // ... and flushed
+  const unsigned cnt = (st1 ? 1u : 0u) + (fl ? 1u : 0u);
+  const unsigned f0 = st1 ? o1 : tp;
+  unsigned *st = stage + so;
+  if (cnt >= 1) st[0] = f0;
+  if (cnt == 2) st[1] = tp;
+  const int disc = (c1 && !in1 ? 1 : 0) + (e2 && !in2 ? 1 : 0) - (x2 && !in1 ? 1 : 0);
+  // dwell at 1: +-edge times by the value before each edge, plus the window
+  // end when the final value is 1 (wrapping arithmetic, exact since the
+  // result lies in [0, wlen])
+  const unsigned e0 = cnt >= 1 ? f0 : 0u, e1 = cnt == 2 ? tp : 0u;
+  const unsigned wf = (cnt & 1u) ? (yy0 ? 0u : wlw) : (yy0 ? wlw : 0u);
+  acc.t1 += (long long)(yy0 ? e0 - e1 + wf : e1 - e0 + wf);
+  T.cnt[w] = cnt;
+  acc.filt += x2 ? 1u : 0u;
+  acc.icf += pairf ? 1u : 0u;
+  acc.disc += disc;
+  if (MODE != MODE_STATS)
+    record_arena<MODE, unsigned>(C, g, base_w + w, (int)cnt, (int)cnt, x2 ? 1 : 0,
+                                 pairf ? 1 : 0, disc, yy0,
+                                 [&](int q) -> unsigned & { return st[q]; });
+}
+
+// ------------------------------------------------------------------ kernel
 // One launch per (logic level, fanin-count group), as gate_eval: persistent
-// grid, work items (gate, run of tiles) fetched from a per-launch counter in
-// tile-group-major order, head items of tpi tiles then tail items of tpi2.
+// grid; work items (gate, run of super-tiles) fetched by the CTA from a
+// per-launch counter in super-tile-group-major order (the CTAs in flight share
+// fanin tiles while they are in L2), head items of tpi super-tiles then tail
+// items of tpi2.
 template <int MODE, int K, bool PCT100>
 __global__ void __launch_bounds__(kEvalThreads, lean_ctas<K>())
 gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
+  constexpr int SLAB = lean_slab_words<K>();
   using SM = LeanSmem<K>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  SM &S = *reinterpret_cast<SM *>(smem_raw);
   const int warp = threadIdx.x / kWarp;
-  SM &S = reinterpret_cast<SM *>(smem_raw)[warp];
+  const int tid = threadIdx.x;
   const unsigned lane = lane_id();
+  LeanWarp<K, SLAB> &T = S.w[warp];
   Region R = region_open(C, (unsigned long long)blockIdx.x * kEvalWarps + warp);
-  if (lane == 0) mbar_init(&S.mbar, 1);
-  __syncwarp();
-  unsigned phase = 0;
+  if (lane == 0) mbar_init(&T.mbar, 1);
+  if (tid < 4) (&S.s.nlist[0][0])[tid] = 0;
+  unsigned phase = 0, par = 0;
+  unsigned *data = reinterpret_cast<unsigned *>(C.data);
+  const int Tw = C.Wpad / 32;
+  const int STc = (C.Tc + kSuper - 1) / kSuper;
   const unsigned head = (unsigned)A.n * (unsigned)A.ntg;
   const unsigned items = head + (unsigned)A.n * (unsigned)A.ntg2;
   while (true) {
-    unsigned it = 0;
-    if (lane == 0) it = atomicAdd(C.work + A.counter, 1u);
-    it = __shfl_sync(0xffffffffu, it, 0);
+    if (tid == 0) S.s.item = atomicAdd(C.work + A.counter, 1u);
+    __syncthreads();
+    const unsigned it = S.s.item;
     if (it >= items) break;
     const bool in_head = it < head;
     const unsigned iq = in_head ? it : it - head;
-    const int j = (int)(iq % (unsigned)A.n);
+    const int jg = (int)(iq % (unsigned)A.n);
     const int tg = (int)(iq / (unsigned)A.n);
-    const int g = __ldg(D.order + A.lo + j);
+    const int g = __ldg(D.order + A.lo + jg);
+    const int gnet = D.P + g;
     const int pin0 = __ldg(D.gate_pin + g);
     const unsigned long long lut = __ldg(D.gate_lut + g);
-    const int t_lo = in_head ? tg * A.tpi : A.ntg * A.tpi + tg * A.tpi2;
-    const int t_hi = min(t_lo + (in_head ? A.tpi : A.tpi2), C.Tc);
+    const int u_lo = in_head ? tg * A.tpi : A.ntg * A.tpi + tg * A.tpi2;
+    const int u_hi = min(u_lo + (in_head ? A.tpi : A.tpi2), STc);
     int net[K], arc[K];
     unsigned ic[K];
 #pragma unroll
@@ -640,19 +445,223 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
       ic[p] = (unsigned)__ldg(D.pin_ic + pin0 + p);
       arc[p] = __ldg(D.pin_arc + pin0 + p);
     }
-    build_dtab<K>(S.arcs, S.dtab, D.arc32, arc);
+    if (warp == 0) build_dtab<K>(S.s.arcs, S.s.dtab, D.arc32, arc);
+    __syncthreads();
     LeanAcc acc;
-    for (int t = t_lo; t < t_hi; ++t)
-      lean_tile<MODE, K, PCT100>(C, g, D.P + g, lut, net, ic, t, A.pct, S, R, phase, acc);
-    acc_flush(C, D.P + g, acc.t1, acc.tc, (long long)acc.filt, (long long)acc.icf,
+    const int t_end = min(u_hi * kSuper, C.Tc);
+    for (int t0 = u_lo * kSuper; t0 < t_end; t0 += kSuper, par ^= 1u) {
+      const int t = t0 + warp;
+      const bool tile = t < t_end;
+      const int base_w = t * kTile;
+      const int nact = tile ? min(kTile, C.Wc - base_w) : 0;
+      const int wl = (int)lane * kWPL;
+      unsigned nib = 0;
+      bool ok = true;
+      // ---- (A) this warp's tile
+      GS_PROF_T(pt0);
+      if (tile) {
+        GS_PROF_ADD(PF_TILES, 1);
+        unsigned c[K][kWPL];
+        unsigned long long tb[K];
+        unsigned bits[K];
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          load_counts(C.cnt + (size_t)net[p] * C.Wpad + base_w + wl, c[p]);
+          tb[p] = __ldg(C.tbase + (size_t)net[p] * C.Tc + t);
+          bits[p] = load_init_bits(C.init + (size_t)net[p] * Tw, t);
+        }
+        unsigned n[kWPL], sidx[kWPL], sso[kWPL], ix[kWPL], p1[kWPL];
+#pragma unroll
+        for (int j = 0; j < kWPL; ++j) n[j] = sidx[j] = sso[j] = ix[j] = p1[j] = 0;
+        unsigned tot[K], seg[K], inw = 0, UB = 0;
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          unsigned s4 = 0;
+#pragma unroll
+          for (int j = 0; j < kWPL; ++j) s4 += c[p][j];
+          unsigned ex = warp_excl_scan(s4, &tot[p]);
+          const unsigned sh = (unsigned)tb[p] & 3u;
+          seg[p] = inw + sh;
+          inw += tot[p] ? (sh + tot[p] + 3u) & ~3u : 0u;
+          UB += tot[p];
+          unsigned o4[kWPL];
+#pragma unroll
+          for (int j = 0; j < kWPL; ++j) {
+            o4[j] = ex;
+            // a one-transition window's single toggle: its pin and slab slot
+            sidx[j] = c[p][j] ? seg[p] + ex : sidx[j];
+            p1[j] = c[p][j] ? (unsigned)p : p1[j];
+            sso[j] += ex;
+            n[j] += c[p][j];
+            ix[j] |= ((bits[p] >> j) & 1u) << p;
+            ex += c[p][j];
+          }
+          st4(&T.offs[p][wl], o4);
+          if (lane == kWarp - 1) T.offs[p][kTile] = tot[p];
+        }
+        // inputs (aligned per pin) and outputs (UB words) in the slab, or both
+        // in global memory
+        const bool in_smem = inw + UB <= (unsigned)SLAB;
+        unsigned *stage;
+        if (in_smem) {
+          if (inw && lane == 0) {
+            fence_proxy_async();  // the slab's earlier generic accesses before the async writes
+            mbar_expect_tx(&T.mbar, inw * 4u);
+#pragma unroll
+            for (int p = 0; p < K; ++p)
+              if (tot[p]) {
+                const unsigned sh = (unsigned)tb[p] & 3u;
+                bulk_g2s(&T.slab[seg[p] - sh], data + (tb[p] - sh),
+                         ((sh + tot[p] + 3u) & ~3u) * 4u, &T.mbar);
+              }
+          }
+          stage = &T.slab[inw];
+        } else {
+          const unsigned long long sb = region_alloc(C, R, UB);
+          ok = sb != ~0ull;
+          stage = data + (ok ? sb : 0ull);
+        }
+        if (lane == 0) {
+          T.in_smem = in_smem ? 1 : 0;
+          T.t = t;
+          T.stage = reinterpret_cast<unsigned long long>(stage);
+#pragma unroll
+          for (int p = 0; p < K; ++p) {
+            T.seg[p] = seg[p];
+            T.tb[p] = tb[p];
+          }
+        }
+        // worklists: two transitions, and three or more (any when in place)
+        const unsigned lim = in_smem ? 1u : 0u;  // windows with n <= lim finish inline
+        unsigned cl = 0;
+#pragma unroll
+        for (int j = 0; j < kWPL; ++j)
+          if (ok && wl + j < nact && n[j] > lim) cl += (n[j] > 2 || !in_smem) ? 1u : 1u << 16;
+        unsigned tot2;
+        const unsigned x = warp_excl_scan(cl, &tot2);
+        unsigned base = 0;
+        if (lane == 0 && tot2) {
+          const unsigned b0 = tot2 & 0xFFFFu ? atomicAdd(&S.s.nlist[par][0], tot2 & 0xFFFFu) : 0u;
+          const unsigned b1 = tot2 >> 16 ? atomicAdd(&S.s.nlist[par][1], tot2 >> 16) : 0u;
+          base = b0 | (b1 << 16);
+        }
+        base = __shfl_sync(0xffffffffu, base, 0);
+        unsigned xl = (base & 0xFFFFu) + (x & 0xFFFFu), xt = (base >> 16) + (x >> 16);
+#pragma unroll
+        for (int j = 0; j < kWPL; ++j)
+          if (ok && wl + j < nact && n[j] > lim) {
+            const bool lp = n[j] > 2 || !in_smem;
+            S.s.list[lp ? 0 : 1][lp ? xl++ : xt++] = wl_entry(wl + j, ix[j], warp);
+          }
+        // the staged segments have landed (all lanes observe the barrier)
+        if (in_smem && inw) {
+          mbar_wait(&T.mbar, phase);
+          phase ^= 1u;
+        }
+        // windows with no transition or one: finished here
+        unsigned oc[kWPL], wl4[kWPL];
+        load_counts(C.wlen32 + base_w + wl, wl4);
+#pragma unroll
+        for (int j = 0; j < kWPL; ++j) {
+          const bool act = ok && wl + j < nact;
+          const bool one = in_smem && n[j] == 1;
+          const unsigned tv = one ? T.slab[one ? sidx[j] : 0u] : 0u;
+          unsigned icp = ic[0];
+#pragma unroll
+          for (int p = 1; p < K; ++p) icp = p1[j] == (unsigned)p ? ic[p] : icp;
+          const unsigned y0 = (unsigned)(lut >> ix[j]) & 1u;
+          const unsigned i1 = ix[j] ^ (1u << p1[j]);
+          const unsigned y1 = (unsigned)(lut >> i1) & 1u;
+          const bool chg = one && y1 != y0;
+          const unsigned ot = tv + icp + dtab_pin<K>(S.s.dtab, p1[j], i1, y1 ? 0u : 1u);
+          const unsigned wln = wl4[j];
+          const bool inwin = ot < wln;
+          const bool st = chg && inwin;
+          const bool inl = act && n[j] <= lim;
+          oc[j] = st ? 1u : 0u;
+          if (st) stage[sso[j]] = ot;
+          acc.disc += (chg && !inwin) ? 1 : 0;
+          acc.t1 += inl ? (y0 ? (st ? ot : wln) : (st ? wln - ot : 0u)) : 0u;
+          nib |= (act ? y0 : 0u) << j;
+          if (MODE != MODE_STATS && inl)
+            record_arena<MODE, unsigned>(C, g, base_w + wl + j, (int)oc[j], (int)oc[j], 0, 0,
+                                         (chg && !inwin) ? 1 : 0, y0,
+                                         [&](int) -> unsigned & { return stage[sso[j]]; });
+          oc[j] = inl ? oc[j] : 0u;  // worklist windows: written in (M)
+        }
+        // counts of the inline windows (worklist windows overwrite theirs)
+        st4(&T.cnt[wl], oc);
+      }
+      GS_PROF_T(pt1);
+      GS_PROF_ADD(PF_PHASE1, pt1 - pt0);
+      __syncthreads();
+      // ---- (M) the pooled worklists of the CTA's tiles
+      {
+        const unsigned nl = S.s.nlist[par][0], n2 = S.s.nlist[par][1];
+        if (tid < 2) S.s.nlist[par ^ 1u][tid] = 0;  // the next step's lists
+        const unsigned L = (nl + kWarp - 1) & ~(unsigned)(kWarp - 1);
+        GS_PROF_ADD(PF_LOOP_WINDOWS, warp == 0 ? nl : 0);
+        GS_PROF_ADD(PF_TRIVIAL, warp == 0 ? n2 : 0);
+        for (unsigned i = tid; i < L + n2; i += kEvalThreads) {
+          if (i < nl) {
+            const unsigned e = S.s.list[0][i];
+            loop_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
+                                               (int)(e & 127u), (e >> 7) & 15u, acc);
+          } else if (i >= L) {
+            const unsigned e = S.s.list[1][i - L];
+            two_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
+                                              (int)(e & 127u), (e >> 7) & 15u, acc);
+          }
+        }
+      }
+      GS_PROF_T(pt2);
+      GS_PROF_ADD(PF_LOOP, pt2 - pt1);
+      __syncthreads();
+      // ---- (C) compaction of this warp's tile and the per-net sums
+      if (tile) {
+        unsigned co[kWPL], so[kWPL], s = 0;
+        ld4(&T.cnt[wl], co);
+        ld4(&T.offs[0][wl], so);
+#pragma unroll
+        for (int p = 1; p < K; ++p) {
+          unsigned o4[kWPL];
+          ld4(&T.offs[p][wl], o4);
+#pragma unroll
+          for (int j = 0; j < kWPL; ++j) so[j] += o4[j];
+        }
+#pragma unroll
+        for (int j = 0; j < kWPL; ++j) {
+          co[j] = (ok && wl + j < nact) ? co[j] : 0u;
+          s += co[j];
+        }
+        unsigned CNT;
+        const unsigned cx = warp_excl_scan(s, &CNT);
+        const unsigned long long ob = CNT ? region_alloc(C, R, CNT) : 0ull;
+        const bool wrote = ob != ~0ull;  // else the chunk is re-run; keep readers in bounds
+        const unsigned *stage = reinterpret_cast<const unsigned *>(T.stage);
+        if (wrote) {
+          unsigned *dst = data + ob + cx;
+#pragma unroll
+          for (int j = 0; j < kWPL; ++j) {
+            const unsigned *sp = stage + so[j];
+            if (co[j] >= 1) dst[0] = sp[0];
+            if (co[j] >= 2) dst[1] = sp[1];
+            for (unsigned q = 2; q < co[j]; ++q) dst[q] = sp[q];
+            dst += co[j];
+          }
+        }
+        acc.tc += s;
+        if (lane == 0) C.tbase[(size_t)gnet * C.Tc + t] = wrote ? ob : 0ull;
+        store_counts(C.cnt + (size_t)gnet * C.Wpad + base_w + wl, co, wrote);
+        store_init_words(C.init + (size_t)gnet * Tw, t, nib);
+      }
+      GS_PROF_T(pt3);
+      GS_PROF_ADD(PF_PHASE3, pt3 - pt2);
+    }
+    acc_flush(C, gnet, acc.t1, acc.tc, (long long)acc.filt, (long long)acc.icf,
               (long long)acc.disc);
   }
   region_close(C, R);
-}
-
-template <int K>
-constexpr size_t lean_smem_bytes() {
-  return sizeof(LeanSmem<K>) * kEvalWarps;
 }
 
 }  // namespace gs

@@ -68,18 +68,34 @@ def allreduce_sum(vec, group=None, device=None):
 def simulate_sharded(model, stimuli, pct=100, group=None, runner=None, device=None,
                      balance=True):
     """Per-net statistics of all windows, computed as this rank's shard plus one
-    all-reduce.  ``runner(w_lo, w_hi) -> (t1, tc, ig, totals)`` defaults to the
-    GPU engine (``simcore.simulate_stats``)."""
+    all-reduce.
+
+    Default (``runner`` None): the GPU engine of this process's device adds
+    the shard's sums into a device int64 buffer ``[t1 | tc | ig | 3 totals]``
+    (``gs_run_stats_device``), the buffer is all-reduced where it lies (NCCL
+    over NVLink with the ``nccl`` backend), and one device-to-host copy
+    returns the merged result.  A ``runner(w_lo, w_hi) -> (t1, tc, ig,
+    totals)`` (host arrays) replaces the engine, e.g. the CPU oracle in the
+    gloo tests.  Returns ``((t1, tc, ig, totals), (lo, hi))``.
+    """
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     W = stimuli.num_windows
     lo, hi = shard_windows(W, world, rank, window_weights(stimuli) if balance else None)
-    if runner is None:
-        from . import simcore
-        runner = lambda a, b: simcore.simulate_stats(model, stimuli, window_range=(a, b),  # noqa
-                                                     pathpulse_pct=pct)
     N = model.num_nets
+    if runner is None:
+        import torch
+        from . import _native, simcore
+        dev = torch.device("cuda", _native.current_device()) if device is None else device
+        acc = torch.zeros(3 * N + 3, dtype=torch.int64, device=dev)
+        if hi > lo:
+            s = simcore._Session.get(model, stimuli)
+            # synchronous on the engine's stream: acc is complete on return
+            s.engine.run_stats_device(s.stim, lo, hi, int(pct), acc.data_ptr())
+        if world > 1:
+            dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+        return unpack(acc.cpu().numpy(), N), (lo, hi)
     if hi > lo:
         vec = pack(*runner(lo, hi))
     else:

@@ -273,6 +273,9 @@ class PassResult:
 
 
 ENGINE_MEM_BUDGET = 0  # device bytes per engine for window-chunk workspace; 0 = 75% of free
+# K4 work-item sizing of new engines (workers, tail_div, tail_frac); None =
+# the engine's defaults.  Tests force the coarse-item and tail paths with it.
+ENGINE_ITEMS = None
 
 
 class _Session:
@@ -284,10 +287,12 @@ class _Session:
         self.design = model.device()
         self.stim = _native.Stimulus(self.design, stimuli)
         self.engine = _native.Engine(self.design, ENGINE_MEM_BUDGET)
+        if ENGINE_ITEMS is not None:
+            self.engine.set_items(*ENGINE_ITEMS)
 
     @classmethod
     def get(cls, model, stimuli):
-        key = (id(model), id(stimuli), ENGINE_MEM_BUDGET)
+        key = (id(model), id(stimuli), ENGINE_MEM_BUDGET, ENGINE_ITEMS)
         s = cls._cache.get(key)
         if s is None or s.model_ref is not model or s.stim_ref is not stimuli:
             cls._cache.clear()  # one live session: device memory is released promptly

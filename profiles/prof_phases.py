@@ -32,16 +32,14 @@ lib.gs_prof_read(buf)
 eng.run_stats(s, 0, W, cfg.pct)
 lib.gs_prof_read(buf)
 v = list(buf)
-names = ["phase1 (counts, staging, ic filter)", "closed form + worklist", "event loop",
-         "phase3 (compaction, dwell)"]
+names = ["(A) counts, staging, inline windows", "(unused)", "(M) pooled worklists",
+         "(C) compaction, sums"]
 tot = sum(v[:4]) or 1
 print(f"config {name} x {W} windows, {cfg.gates} gates")
 for i, n in enumerate(names):
     print(f"  {n:40s} {v[i] / tot * 100:5.1f}% of warp-cycles")
 tiles = max(v[8], 1)
-print(f"  tiles {v[8]}, in-place (slow) tiles {v[10]}, closed-form windows {v[9]} "
+print(f"  tiles {v[8]}, two-transition windows {v[9]} "
       f"({v[9] / (tiles * 128) * 100:.1f}% of tile windows), loop windows {v[7]} "
       f"({v[7] / (tiles * 128) * 100:.1f}%)")
-print(f"  loop iterations {v[4]}, busy lanes/iter {v[5] / max(v[4], 1):.2f}, "
-      f"iterations per tile {v[4] / tiles:.2f}")
 print(f"  device ms (gate_eval) {eng.timing()['ms_gate_eval']:.2f}")

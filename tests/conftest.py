@@ -41,3 +41,4 @@ def oracle_lib():
     from oracle import port
     port.build()
     return port
+collect_ignore = ["reference_suite"]

@@ -85,3 +85,58 @@ def test_two_rank_gloo_allreduce_equals_single_run(oracle_lib):
         assert np.array_equal(r[5], full["ig"])
         assert r[6] == (int(arena["filtered"].sum()), int(arena["ic_filtered"].sum()),
                         int(arena["discarded"].sum()))
+
+
+def _gpu_rank(rank, world, port, q):
+    # both ranks drive the GPU engine on cuda:0 (one GPU in this pool); they
+    # never wait on each other on the device: the sums go through gloo
+    import torch.distributed as dist
+    import gen
+    import paper_2203_06117_b200 as api
+    from paper_2203_06117_b200 import synth
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = []
+    docs = gen.make_docs(4242, n_gates=400, n_pis=8, windows=40, duration_ps=20_000,
+                         max_toggles=300)
+    nl, lv, delays, waves, duration, b, stim = gen.load(docs, api)
+    model = api.compile_design(lv, delays)
+    out.append(distributed.simulate_sharded(model, stim, docs.pct))
+    cfg = synth.config("C2", gates=20_000, windows=700)
+    m = synth.design(cfg)
+    out.append(distributed.simulate_sharded(m, synth.stimulus(cfg, 0, 700), cfg.pct))
+    q.put((rank, [((list(map(np.asarray, r[0][:3])), r[0][3]), r[1]) for r in out]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_two_rank_gpu_runner_equals_single_run():
+    import gen
+    import paper_2203_06117_b200 as api
+    from paper_2203_06117_b200 import synth
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_gpu_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=500) for _ in range(2)), key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+    docs = gen.make_docs(4242, n_gates=400, n_pis=8, windows=40, duration_ps=20_000,
+                         max_toggles=300)
+    nl, lv, delays, waves, duration, b, stim = gen.load(docs, api)
+    single = [api.simulate_stats(api.compile_design(lv, delays), stim,
+                                 pathpulse_pct=docs.pct)]
+    cfg = synth.config("C2", gates=20_000, windows=700)
+    single.append(api.simulate_stats(synth.design(cfg), synth.stimulus(cfg, 0, 700),
+                                     pathpulse_pct=cfg.pct))
+    for case, ref in enumerate(single):
+        shards = [res[r][1][case][1] for r in range(2)]
+        assert shards[0][0] == 0 and shards[0][1] == shards[1][0] < shards[1][1]
+        for r in range(2):
+            (arrs, totals), _ = res[r][1][case]
+            for a, x in zip(arrs, ref[:3]):
+                assert np.array_equal(a, x)
+            assert tuple(totals) == tuple(ref[3])
