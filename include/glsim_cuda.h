@@ -170,6 +170,10 @@ int gs_engine_destroy(gs_engine *e);
  * divisor the tail items are re-cut by (1 = no tail re-cut) and the largest
  * tail share 1/tail_frac of a launch's columns.  Results never depend on it. */
 int gs_engine_set_items(gs_engine *e, int64_t workers, int tail_div, int tail_frac);
+/* words per warp of the shared-memory slab that stages a tile's fanin
+ * segments and outputs in the K4 instance for k-input gates (narrow != 0:
+ * 32-bit window-relative time); tiles that do not fit read in place */
+int gs_slab_words(int k, int narrow);
 
 /* Stats run over windows [w_lo, w_hi): K1 stim_segment + per level K4
  * gate_eval with the dwell/toggle reduction fused (replaces count_pass +
@@ -300,6 +304,32 @@ int gs_saif_format(const char *names, const int64_t *name_off, int64_t num_nets,
                    const int64_t *t0, const int64_t *t1, const int64_t *tc, const int64_t *ig,
                    int64_t duration, const char *design_name, const char *saif_version,
                    int include_ig, char *out, int64_t out_cap, int64_t *out_len);
+
+/* VcdWriter / write_vcd (pkg/src/glsim/report.py:144-214): the byte-exact VCD
+ * dump of simulated waveforms.  gs_vcdw_create writes the header for the
+ * listed net names (UTF-8 in `names`, byte offsets name_off [num_names+1]);
+ * each gs_vcdw_feed appends windows [w_lo, w_hi) of every listed net -- net i
+ * is row net_row[i] of waveform source src[net_src[i]] (0: primary inputs,
+ * 1: gates; windowed int64 arrays, absolute times) -- keeping each name's
+ * last value across feeds; gs_vcdw_finish appends the end time.  The text
+ * accumulates in the handle: gs_vcdw_take copies it out (buf NULL: size only)
+ * and clears it. */
+typedef struct gs_wave_src {
+  const int64_t *buf;
+  int64_t n_buf;
+  const int64_t *offsets, *counts;  /* [rows, cols] */
+  const uint8_t *initials;          /* [rows, cols] */
+  int64_t cols;                     /* row pitch (windows) */
+  int64_t col0;                     /* column of window w_lo */
+} gs_wave_src;
+typedef struct gs_vcdw gs_vcdw;
+int gs_vcdw_create(const char *names, const int64_t *name_off, int64_t num_names,
+                   const char *design_name, gs_vcdw **out);
+int gs_vcdw_feed(gs_vcdw *w, const uint8_t *net_src, const int64_t *net_row,
+                 const gs_wave_src *src, const int64_t *boundaries, int64_t w_lo, int64_t w_hi);
+int gs_vcdw_finish(gs_vcdw *w, int64_t end_time);
+int gs_vcdw_take(gs_vcdw *w, char *buf, int64_t cap, int64_t *len);
+int gs_vcdw_destroy(gs_vcdw *w);
 
 #ifdef __cplusplus
 }

@@ -68,6 +68,11 @@ class SdfDesign(C.Structure):
                 ("out_net", _i64p)]
 
 
+class WaveSrc(C.Structure):
+    _fields_ = [("buf", _i64p), ("n_buf", C.c_int64), ("offsets", _i64p), ("counts", _i64p),
+                ("initials", _u8p), ("cols", C.c_int64), ("col0", C.c_int64)]
+
+
 class ArenaRef(C.Structure):
     _fields_ = [("buf", _i64p), ("n_buf", C.c_int64), ("offsets", _i64p), ("counts", _i64p),
                 ("initials", _u8p), ("cols", C.c_int64)]
@@ -96,6 +101,7 @@ SIGNATURES = {
     "gs_engine_create": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(C.c_void_p)]),
     "gs_engine_destroy": (C.c_int, [C.c_void_p]),
     "gs_engine_set_items": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_int]),
+    "gs_slab_words": (C.c_int, [C.c_int, C.c_int]),
     "gs_run_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
                                C.POINTER(StatsOut)]),
     "gs_run_arena": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
@@ -123,6 +129,13 @@ SIGNATURES = {
     "gs_sdf_copy": (C.c_int, [C.c_void_p, _i64p, _i64p]),
     "gs_sdf_warning": (C.c_char_p, [C.c_void_p, C.c_int64]),
     "gs_sdf_destroy": (C.c_int, [C.c_void_p]),
+    "gs_vcdw_create": (C.c_int, [C.c_char_p, _i64p, C.c_int64, C.c_char_p,
+                                 C.POINTER(C.c_void_p)]),
+    "gs_vcdw_feed": (C.c_int, [C.c_void_p, _u8p, _i64p, C.POINTER(WaveSrc), _i64p, C.c_int64,
+                               C.c_int64]),
+    "gs_vcdw_finish": (C.c_int, [C.c_void_p, C.c_int64]),
+    "gs_vcdw_take": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, _i64p]),
+    "gs_vcdw_destroy": (C.c_int, [C.c_void_p]),
     "gs_saif_format": (C.c_int, [C.c_char_p, _i64p, C.c_int64, _i64p, _i64p, _i64p, _i64p,
                                  C.c_int64, C.c_char_p, C.c_char_p, C.c_int, C.c_char_p,
                                  C.c_int64, _i64p]),
@@ -330,6 +343,51 @@ def saif_format(net_names, t0, t1, tc, ig, duration, design_name, version, inclu
     n = C.c_int64()
     _check(lib.gs_saif_format(*args, buf.ctypes.data_as(C.c_char_p), need.value, C.byref(n)))
     return buf[:n.value].tobytes().decode("utf-8", errors="surrogatepass")
+
+
+class VcdText:
+    """Native VCD writer handle (``gs_vcdw_*``): header on creation, windows
+    appended by :meth:`feed`; :meth:`take` returns the pending text."""
+
+    def __init__(self, names, design_name):
+        lib = load()
+        blob, off = _blob(names)
+        h = C.c_void_p()
+        _check(lib.gs_vcdw_create(blob, _p64(off), len(off) - 1,
+                                  str(design_name).encode("utf-8", errors="surrogatepass"),
+                                  C.byref(h)))
+        self.handle = h
+        self._fin = weakref.finalize(self, lib.gs_vcdw_destroy, h)
+
+    @staticmethod
+    def _src(buf, offsets, counts, initials, col0):
+        keep = (_c64(buf), _c64(offsets), _c64(counts), _c8(initials))
+        b, o, c, i = keep
+        cols = o.shape[1] if o.ndim == 2 else 0
+        s = WaveSrc(buf=_p64(b) if b.size else None, n_buf=b.size, offsets=_p64(o),
+                    counts=_p64(c), initials=_p8(i), cols=cols, col0=int(col0))
+        return s, keep
+
+    def feed(self, net_src, net_row, inputs, gates, boundaries, w_lo, w_hi):
+        """``inputs`` / ``gates``: (buf, offsets, counts, initials, col0) windowed
+        arrays; net i is row net_row[i] of inputs (net_src 0) or gates (1)."""
+        s0, k0 = self._src(*inputs)
+        s1, k1 = self._src(*gates)
+        srcs = (WaveSrc * 2)(s0, s1)
+        ns, nr, b = _c8(net_src), _c64(net_row), _c64(boundaries)
+        _check(load().gs_vcdw_feed(self.handle, _p8(ns), _p64(nr), srcs, _p64(b), int(w_lo),
+                                   int(w_hi)))
+
+    def finish(self, end_time):
+        _check(load().gs_vcdw_finish(self.handle, int(end_time)))
+
+    def take(self):
+        lib = load()
+        n = C.c_int64()
+        _check(lib.gs_vcdw_take(self.handle, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(max(1, n.value))
+        _check(lib.gs_vcdw_take(self.handle, buf, n.value, C.byref(n)))
+        return buf.raw[:n.value].decode("utf-8", errors="surrogatepass")
 
 
 def _p64(a):

@@ -17,6 +17,7 @@
 #include "kernels_lean.cuh"
 #include "synth.cuh"
 #include "vcd_reader.h"
+#include "vcd_writer.h"
 #include "sdf_reader.h"
 
 using namespace gs;
@@ -615,6 +616,7 @@ int64_t meta_bytes_per_window(const gs_design *d, bool arena) {
 // profiles/ab_tail.sh, round 1: C2 -3.0 %, C3 -0.7 %).
 constexpr int kItemCap = 12;   // tiles per item (profiles/ab_items_r01.log)
 constexpr int kItemDiv = 4;
+constexpr int kLeanItemCap = 8;  // super-tiles (of 4 tiles) per item of the lean kernels
 
 struct ItemPlan {
   int tpi, ntg, tpi2, ntg2;
@@ -810,7 +812,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
         const ItemPlan ip = plan_items(n, lean ? STc : Tc,
                                        e->item_workers > 0 ? e->item_workers
                                                            : (lean ? ncta : nregions),
-                                       lean ? kItemCap / kSuper : kItemCap, e->tail_div,
+                                       lean ? kLeanItemCap : kItemCap, e->tail_div,
                                        e->tail_frac);
         A.tpi = ip.tpi;
         A.ntg = ip.ntg;
@@ -1185,6 +1187,16 @@ int gs_engine_create(gs_design *d, int64_t mem_budget, void *stream, gs_engine *
   }
   *out = e;
   return GS_OK;
+}
+
+int gs_slab_words(int k, int narrow) {
+  // words of a warp's shared-memory slab in the K4 instance that evaluates
+  // k-input gates (narrow: 32-bit time); a tile's fanin segments and outputs
+  // are staged there when they fit
+  if (narrow && k >= 1 && k <= 4)
+    return k == 1 ? lean_slab_words<1>() : k == 2 ? lean_slab_words<2>()
+         : k == 3 ? lean_slab_words<3>() : lean_slab_words<4>();
+  return slab_words<0>();
 }
 
 int gs_engine_set_items(gs_engine *e, int64_t workers, int tail_div, int tail_frac) {
@@ -1636,6 +1648,79 @@ int gs_saif_format(const char *names, const int64_t *name_off, int64_t num_nets,
   }
   put(tail, sizeof(tail) - 1);
   *out_len = p - out;
+  return GS_OK;
+}
+
+}  // extern "C"
+
+// =========================================================================
+// VCD writer (report.py:144-214)
+
+struct gs_vcdw {
+  gsvcd::NameTable names;
+  std::vector<int8_t> last;
+  std::string text;
+  int64_t num = 0;
+};
+
+extern "C" {
+
+int gs_vcdw_create(const char *names, const int64_t *name_off, int64_t num_names,
+                   const char *design_name, gs_vcdw **out) {
+  if (!out || num_names < 0 || (num_names && (!names || !name_off)) || !design_name)
+    return fail(GS_ERR_ARG, "bad VCD writer arguments");
+  *out = nullptr;
+  for (int64_t i = 0; i < num_names; ++i)
+    if (name_off[i + 1] < name_off[i]) return fail(GS_ERR_ARG, "name offsets not monotone");
+  gs_vcdw *w = new gs_vcdw();
+  w->num = num_names;
+  w->names.build(names, name_off, num_names);
+  w->last.assign(w->names.id.size(), (int8_t)-1);
+  gsvcd::header(w->text, names, name_off, num_names, w->names, design_name);
+  *out = w;
+  return GS_OK;
+}
+
+int gs_vcdw_feed(gs_vcdw *w, const uint8_t *net_src, const int64_t *net_row,
+                 const gs_wave_src *src, const int64_t *boundaries, int64_t w_lo, int64_t w_hi) {
+  if (!w || !src || !boundaries || w_hi < w_lo || (w->num && (!net_src || !net_row)))
+    return fail(GS_ERR_ARG, "bad VCD feed arguments");
+  gsvcd::Source S[2];
+  for (int k = 0; k < 2; ++k)
+    S[k] = {src[k].buf, src[k].offsets, src[k].counts, src[k].initials, src[k].cols,
+            src[k].col0, src[k].n_buf};
+  for (int64_t i = 0; i < w->num; ++i) {
+    const gsvcd::Source &q = S[net_src[i] ? 1 : 0];
+    if (!q.offsets || !q.counts || !q.initials || net_row[i] < 0 || q.col0 < 0 ||
+        q.col0 + (w_hi - w_lo) > q.cols)
+      return fail(GS_ERR_ARG, "VCD feed: waveform source does not cover the net / windows");
+  }
+  if (!gsvcd::feed(w->text, w->num, net_src, net_row, S, boundaries, w_lo, w_hi, w->names,
+                   w->last))
+    return fail(GS_ERR_ARG, "VCD feed: waveform region outside its buffer");
+  return GS_OK;
+}
+
+int gs_vcdw_finish(gs_vcdw *w, int64_t end_time) {
+  if (!w) return fail(GS_ERR_ARG, "null VCD writer");
+  w->text.push_back('#');
+  gsvcd::put_int(w->text, end_time);
+  w->text.push_back('\n');
+  return GS_OK;
+}
+
+int gs_vcdw_take(gs_vcdw *w, char *buf, int64_t cap, int64_t *len) {
+  if (!w || !len) return fail(GS_ERR_ARG, "bad VCD take arguments");
+  *len = (int64_t)w->text.size();
+  if (!buf) return GS_OK;
+  if (cap < *len) return fail(GS_ERR_ARG, "VCD text buffer too small");
+  memcpy(buf, w->text.data(), w->text.size());
+  w->text.clear();
+  return GS_OK;
+}
+
+int gs_vcdw_destroy(gs_vcdw *w) {
+  delete w;
   return GS_OK;
 }
 

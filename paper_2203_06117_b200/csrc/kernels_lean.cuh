@@ -531,28 +531,38 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
             T.tb[p] = tb[p];
           }
         }
-        // worklists: two transitions, and three or more (any when in place)
-        const unsigned lim = in_smem ? 1u : 0u;  // windows with n <= lim finish inline
-        unsigned cl = 0;
+        // worklists: two transitions, and three or more (any when in place);
+        // positions by warp ballots, one shared-memory atomic per list
+        unsigned amask = 0;  // the lane's windows inside the chunk
 #pragma unroll
-        for (int j = 0; j < kWPL; ++j)
-          if (ok && wl + j < nact && n[j] > lim) cl += (n[j] > 2 || !in_smem) ? 1u : 1u << 16;
-        unsigned tot2;
-        const unsigned x = warp_excl_scan(cl, &tot2);
+        for (int j = 0; j < kWPL; ++j) amask |= (ok && wl + j < nact ? 1u : 0u) << j;
+        const unsigned lim = in_smem ? 1u : 0u;  // windows with n <= lim finish inline
+        const unsigned lt = (1u << lane) - 1u;
+        unsigned bl[kWPL], bt[kWPL], nL = 0, nT = 0;
+#pragma unroll
+        for (int j = 0; j < kWPL; ++j) {
+          const bool a = (amask >> j) & 1u;
+          bl[j] = __ballot_sync(0xffffffffu, a && n[j] > lim && (n[j] > 2 || !in_smem));
+          bt[j] = __ballot_sync(0xffffffffu, a && in_smem && n[j] == 2);
+          nL += __popc(bl[j]);
+          nT += __popc(bt[j]);
+        }
         unsigned base = 0;
-        if (lane == 0 && tot2) {
-          const unsigned b0 = tot2 & 0xFFFFu ? atomicAdd(&S.s.nlist[par][0], tot2 & 0xFFFFu) : 0u;
-          const unsigned b1 = tot2 >> 16 ? atomicAdd(&S.s.nlist[par][1], tot2 >> 16) : 0u;
+        if (lane == 0) {
+          const unsigned b0 = nL ? atomicAdd(&S.s.nlist[par][0], nL) : 0u;
+          const unsigned b1 = nT ? atomicAdd(&S.s.nlist[par][1], nT) : 0u;
           base = b0 | (b1 << 16);
         }
         base = __shfl_sync(0xffffffffu, base, 0);
-        unsigned xl = (base & 0xFFFFu) + (x & 0xFFFFu), xt = (base >> 16) + (x >> 16);
+        unsigned xl = base & 0xFFFFu, xt = base >> 16;
 #pragma unroll
-        for (int j = 0; j < kWPL; ++j)
-          if (ok && wl + j < nact && n[j] > lim) {
-            const bool lp = n[j] > 2 || !in_smem;
-            S.s.list[lp ? 0 : 1][lp ? xl++ : xt++] = wl_entry(wl + j, ix[j], warp);
-          }
+        for (int j = 0; j < kWPL; ++j) {
+          const unsigned short e = wl_entry(wl + j, ix[j], warp);
+          if ((bl[j] >> lane) & 1u) S.s.list[0][xl + __popc(bl[j] & lt)] = e;
+          if ((bt[j] >> lane) & 1u) S.s.list[1][xt + __popc(bt[j] & lt)] = e;
+          xl += __popc(bl[j]);
+          xt += __popc(bt[j]);
+        }
         // the staged segments have landed (all lanes observe the barrier)
         if (in_smem && inw) {
           mbar_wait(&T.mbar, phase);
@@ -563,7 +573,7 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         load_counts(C.wlen32 + base_w + wl, wl4);
 #pragma unroll
         for (int j = 0; j < kWPL; ++j) {
-          const bool act = ok && wl + j < nact;
+          const bool act = (amask >> j) & 1u;
           const bool one = in_smem && n[j] == 1;
           const unsigned tv = one ? T.slab[one ? sidx[j] : 0u] : 0u;
           unsigned icp = ic[0];
@@ -578,16 +588,19 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
           const bool inwin = ot < wln;
           const bool st = chg && inwin;
           const bool inl = act && n[j] <= lim;
-          oc[j] = st ? 1u : 0u;
           if (st) stage[sso[j]] = ot;
           acc.disc += (chg && !inwin) ? 1 : 0;
-          acc.t1 += inl ? (y0 ? (st ? ot : wln) : (st ? wln - ot : 0u)) : 0u;
+          // dwell at 1: the start value holds until the stored edge (or the
+          // window end), the other value after it
+          const unsigned e = st ? ot : wln;
+          const unsigned dw = y0 ? e : wln - e;
+          acc.t1 += inl ? dw : 0u;
           nib |= (act ? y0 : 0u) << j;
           if (MODE != MODE_STATS && inl)
-            record_arena<MODE, unsigned>(C, g, base_w + wl + j, (int)oc[j], (int)oc[j], 0, 0,
+            record_arena<MODE, unsigned>(C, g, base_w + wl + j, st ? 1 : 0, st ? 1 : 0, 0, 0,
                                          (chg && !inwin) ? 1 : 0, y0,
                                          [&](int) -> unsigned & { return stage[sso[j]]; });
-          oc[j] = inl ? oc[j] : 0u;  // worklist windows: written in (M)
+          oc[j] = inl && st ? 1u : 0u;  // worklist windows: written in (M)
         }
         // counts of the inline windows (worklist windows overwrite theirs)
         st4(&T.cnt[wl], oc);
@@ -620,6 +633,9 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
       // ---- (C) compaction of this warp's tile and the per-net sums
       if (tile) {
         unsigned co[kWPL], so[kWPL], s = 0;
+        unsigned amask = 0;
+#pragma unroll
+        for (int j = 0; j < kWPL; ++j) amask |= (ok && wl + j < nact ? 1u : 0u) << j;
         ld4(&T.cnt[wl], co);
         ld4(&T.offs[0][wl], so);
 #pragma unroll
@@ -631,7 +647,7 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         }
 #pragma unroll
         for (int j = 0; j < kWPL; ++j) {
-          co[j] = (ok && wl + j < nact) ? co[j] : 0u;
+          co[j] = (amask >> j) & 1u ? co[j] : 0u;
           s += co[j];
         }
         unsigned CNT;

@@ -90,6 +90,7 @@ def run_case(ref, docs):
         pin_net=model.pin_net, pin_ic=model.pin_ic, pin_arc=model.pin_arc,
         arc_rows=model.arc_rows,
         saif=np.frombuffer(ref.write_saif(stats, nl.name).encode(), dtype=np.uint8),
+        vcd_out=np.frombuffer(ref.write_vcd(arena, stimuli=stim).encode(), dtype=np.uint8),
         report=np.frombuffer(json.dumps({k: v for k, v in ref.run_report(stats, diag).items()
                                          if k not in ("timings", "tasks")}).encode(),
                              dtype=np.uint8),
