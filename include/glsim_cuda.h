@@ -193,6 +193,18 @@ int gs_run_arena(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct,
 
 int gs_last_timing(gs_engine *e, gs_timing *t);
 
+/* The arena buffer of the last count pass (gs_run_arena with buf == NULL) on
+ * this engine, without a second simulation: the count pass keeps every
+ * gate-window's peak entries (K5 packs them per window chunk, gate-major in
+ * level order, absolute int64 times); this scatters them into `buf` at the
+ * regions `offsets` [G, cols] (allocate_arena's layout, waveform.py:321-346)
+ * -- the contents store_pass (simcore.py:382-410) would write.  *filled = 0
+ * (and nothing written) unless the engine's last count pass was this
+ * stimulus, window range and pct. */
+int gs_arena_fill(gs_engine *e, const gs_stim *s, int64_t w_lo, int64_t w_hi, int pct,
+                  int64_t *buf, int64_t n_buf, const int64_t *offsets, int64_t cols,
+                  int *filled);
+
 /* Device-side stats accumulation for multi-GPU reduction: like gs_run_stats
  * but ADDS into a caller-owned device buffer acc_dev of 3*N+3 int64
  * ([t1 | tc | ig | filtered, ic_filtered, discarded]), so the caller can

@@ -107,6 +107,8 @@ SIGNATURES = {
     "gs_run_arena": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
                                C.POINTER(ArenaOut), C.POINTER(StatsOut)]),
     "gs_last_timing": (C.c_int, [C.c_void_p, C.POINTER(Timing)]),
+    "gs_arena_fill": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int, _i64p,
+                                C.c_int64, _i64p, C.c_int64, C.POINTER(C.c_int)]),
     "gs_run_stats_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
                                       C.c_void_p]),
     "gs_run_compare": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
@@ -615,6 +617,18 @@ class Engine:
         if want_stats:
             res["stats"] = (t1, tc, ig, tuple(int(x) for x in st.totals))
         return res
+
+    def arena_fill(self, stim, w_lo, w_hi, pct, buf, offsets):
+        """Fill ``buf`` at ``offsets`` [G, Ws] from this engine's last count
+        pass of (stim, [w_lo, w_hi), pct) (``gs_arena_fill``); False (nothing
+        written) when that pass is not the last one run."""
+        off = _c64(offsets)
+        f = C.c_int(0)
+        _check(load().gs_arena_fill(self.handle, stim.handle, int(w_lo), int(w_hi), int(pct),
+                                    _p64(buf) if buf.size else None, buf.size, _p64(off),
+                                    off.shape[1] if off.ndim == 2 else int(w_hi) - int(w_lo),
+                                    C.byref(f)))
+        return bool(f.value)
 
     def timing(self):
         t = Timing()

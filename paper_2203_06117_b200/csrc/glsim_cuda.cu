@@ -16,6 +16,7 @@
 #include "kernels.cuh"
 #include "kernels_lean.cuh"
 #include "synth.cuh"
+#include "arena.cuh"
 #include "vcd_reader.h"
 #include "vcd_writer.h"
 #include "sdf_reader.h"
@@ -172,6 +173,8 @@ struct gs_design {
   unsigned *arc32 = nullptr;
   unsigned long long *gate_lut = nullptr;
   unsigned *lut_words = nullptr;
+  int *order_ref = nullptr;          // the arena order (levelized order as given)
+  std::vector<int> order_host;
 
   DesignDev dev() const {
     DesignDev D;
@@ -193,6 +196,7 @@ struct gs_design {
   void release() {
     dfree(order); dfree(gate_k); dfree(gate_pin); dfree(pin_net); dfree(pin_arc);
     dfree(pin_ic); dfree(arc); dfree(arc32); dfree(gate_lut); dfree(lut_words);
+    dfree(order_ref);
   }
 };
 
@@ -297,6 +301,8 @@ static int design_build(const gs_design_desc *d, int device, gs_design *D) {
   }
   TRY(use_device(device));
   TRY(upload(&D->order, order.data(), G));
+  D->order_host.assign(d->order, d->order + G);
+  TRY(upload(&D->order_ref, D->order_host.data(), G));
   TRY(upload(&D->gate_k, D->k_of.data(), G));
   TRY(upload(&D->gate_pin, gate_pin.data(), G));
   TRY(upload(&D->gate_lut, gate_lut.data(), G));
@@ -441,7 +447,20 @@ struct gs_engine {
   long long *a_cnt = nullptr, *a_peak = nullptr, *a_filt = nullptr, *a_icf = nullptr,
             *a_disc = nullptr, *a_off = nullptr, *a_buf = nullptr;
   unsigned char *a_init = nullptr;
+  unsigned long long *a_pos = nullptr;
   int64_t a_buf_cap = 0;
+  // K5: the last count pass's packed arena pieces, one per window chunk
+  struct ArenaPiece {
+    int64_t w0, wc;
+    std::vector<int64_t> rs;      // [G] entries per gate in the chunk
+    std::vector<int64_t> piece;   // gate-major (arena order), absolute times
+  };
+  std::vector<ArenaPiece> kept;
+  const gs_stim *kept_stim = nullptr;
+  int64_t kept_lo = 0, kept_hi = 0;
+  int kept_pct = -1;
+  long long *k5_rs = nullptr, *k5_base = nullptr, *k5_part = nullptr, *k5_out = nullptr;
+  int64_t k5_out_cap = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t chunk_hint[2] = {0, 0};   // per mode family: stats, arena
   // work-item sizing (gs_engine_set_items): workers assumed (0 = the grid),
@@ -453,12 +472,13 @@ struct gs_engine {
   void release_meta() { dfree(cnt); dfree(tbase); dfree(init); dfree(wlen32); meta_windows = 0; }
   void release_arena() {
     dfree(a_cnt); dfree(a_peak); dfree(a_filt); dfree(a_icf); dfree(a_disc); dfree(a_off);
-    dfree(a_init); arena_windows = 0;
+    dfree(a_init); dfree(a_pos); arena_windows = 0;
   }
   void release() {
     release_meta();
     release_arena();
     dfree(a_buf);
+    dfree(k5_rs); dfree(k5_base); dfree(k5_part); dfree(k5_out);
     dfree(data);
     dfree(bump);
     dfree(work);
@@ -565,7 +585,7 @@ int ensure_meta(gs_engine *e, int64_t wins) {
   const int64_t N = e->d->N;
   const int64_t Wpad = round_up(wins, kTile);
   TRY(dalloc(&e->cnt, (size_t)(N * Wpad)));
-  TRY(dalloc(&e->tbase, (size_t)(N * (Wpad / kTile))));
+  TRY(dalloc(&e->tbase, (size_t)(N * (Wpad / kTile)) + 2));  // +2: aligned 16-byte prefetch pieces
   TRY(dalloc(&e->init, (size_t)(N * (Wpad / 32))));
   TRY(dalloc(&e->wlen32, (size_t)Wpad));
   e->meta_windows = Wpad;
@@ -583,6 +603,7 @@ int ensure_arena(gs_engine *e, int64_t wins, bool store) {
   TRY(dalloc(&e->a_disc, n));
   TRY(dalloc(&e->a_init, n));
   TRY(dalloc(&e->a_off, n));
+  TRY(dalloc(&e->a_pos, n));
   e->arena_windows = round_up(wins, kTile);
   return GS_OK;
 }
@@ -655,6 +676,53 @@ struct RunOut {
   int64_t arena_cols;       // Ws (host row pitch)
   CompareDev *cmp = nullptr;  // device cross-check against a reference arena (K7)
 };
+
+// K5: the chunk's gate waveforms (peak entries per window, as the count pass
+// left them in the pool) packed gate-major in arena order, absolute int64,
+// and kept on the host with the per-gate entry counts for gs_arena_fill.
+template <typename TS>
+int k5_pack(gs_engine *e, const ChunkDev &C, int64_t w0, int64_t wc) {
+  gs_design *D = e->d;
+  const int G = D->G;
+  gs_engine::ArenaPiece pc;
+  pc.w0 = w0;
+  pc.wc = wc;
+  pc.rs.assign(G, 0);
+  if (G > 0) {
+    const int nb = (G + kScanBlock - 1) / kScanBlock;
+    if (!e->k5_rs) {
+      TRY(dalloc(&e->k5_rs, (size_t)G));
+      TRY(dalloc(&e->k5_base, (size_t)G));
+      TRY(dalloc(&e->k5_part, (size_t)nb + 1));
+    }
+    const int blocks = (int)std::min<int64_t>((G + 7) / 8, (int64_t)e->sms * 16);
+    arena_rowsum<<<blocks, 256, 0, e->st>>>(C.a_peak, G, C.Wc, C.Wpad, e->k5_rs);
+    scan_blocks<<<nb, kScanThreads, 0, e->st>>>(e->k5_rs, D->order_ref, G, e->k5_base, e->k5_part);
+    scan_parts<<<1, 1024, 0, e->st>>>(e->k5_part, nb);
+    scan_add<<<nb, kScanThreads, 0, e->st>>>(e->k5_base, D->order_ref, G, e->k5_part);
+    CK(cudaGetLastError());
+    long long total = 0;
+    CK(cudaMemcpyAsync(&total, e->k5_part + nb, sizeof(long long), cudaMemcpyDeviceToHost, e->st));
+    CK(cudaMemcpyAsync(pc.rs.data(), e->k5_rs, sizeof(long long) * G, cudaMemcpyDeviceToHost, e->st));
+    CK(cudaStreamSynchronize(e->st));
+    if (total > e->k5_out_cap) {
+      dfree(e->k5_out);
+      e->k5_out_cap = 0;
+      TRY(dalloc(&e->k5_out, (size_t)total));
+      e->k5_out_cap = total;
+    }
+    if (total) {
+      arena_pack<TS><<<blocks, 256, 0, e->st>>>(C, G, e->k5_base, e->k5_out);
+      CK(cudaGetLastError());
+      pc.piece.resize((size_t)total);
+      CK(cudaMemcpyAsync(pc.piece.data(), e->k5_out, sizeof(long long) * total,
+                         cudaMemcpyDeviceToHost, e->st));
+      CK(cudaStreamSynchronize(e->st));
+    }
+  }
+  e->kept.push_back(std::move(pc));
+  return GS_OK;
+}
 
 template <typename TS, int MODE>
 int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, RunOut &ro) {
@@ -764,6 +832,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
       C.a_off = e->a_off;
       C.a_buf = e->a_buf;
       C.a_nbuf = store ? ro.arena->n_buf : 0;
+      C.a_pos = e->a_pos;
       if (store) {
         CK(cudaMemcpy2DAsync(e->a_off, Wpad * 8, ro.arena->offsets + (w - ro.w_base),
                              ro.arena_cols * 8, wc * 8, G, cudaMemcpyHostToDevice, e->st));
@@ -896,6 +965,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
         CK(cudaMemcpy2DAsync(ar->initials + col, ro.arena_cols, e->a_init, Wpad, wc, G,
                              cudaMemcpyDeviceToHost, e->st));
       CK(cudaStreamSynchronize(e->st));
+      if (!store) TRY(k5_pack<TS>(e, C, w, wc));
     }
     // adapt: a pool well under-filled lets the next chunk grow, but never
     // past the metadata share of the budget the first chunk was sized by
@@ -1302,9 +1372,48 @@ int gs_run_arena(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct,
   }
   CK(cudaMemsetAsync(e->acc_run, 0, sizeof(long long) * (3 * (size_t)e->d->N + 3), e->st));
   RunOut ro{e->acc_run, arena, w_lo, w_hi - w_lo};
-  if (store) TRY(run_mode<MODE_STORE>(e, s, w_lo, w_hi, pct, ro));
-  else TRY(run_mode<MODE_COUNTERS>(e, s, w_lo, w_hi, pct, ro));
+  e->kept.clear();
+  e->kept_stim = nullptr;
+  if (store) {
+    TRY(run_mode<MODE_STORE>(e, s, w_lo, w_hi, pct, ro));
+  } else {
+    TRY(run_mode<MODE_COUNTERS>(e, s, w_lo, w_hi, pct, ro));
+    e->kept_stim = s;
+    e->kept_lo = w_lo;
+    e->kept_hi = w_hi;
+    e->kept_pct = pct;
+  }
   if (stats) return finish_stats(e, stats);
+  return GS_OK;
+}
+
+int gs_arena_fill(gs_engine *e, const gs_stim *s, int64_t w_lo, int64_t w_hi, int pct,
+                  int64_t *buf, int64_t n_buf, const int64_t *offsets, int64_t cols,
+                  int *filled) {
+  if (!e || !filled || (!buf && n_buf) || cols < w_hi - w_lo || n_buf < 0)
+    return fail(GS_ERR_ARG, "bad arena fill arguments");
+  *filled = 0;
+  if (!e->kept_stim || e->kept_stim != s || e->kept_lo != w_lo || e->kept_hi != w_hi ||
+      e->kept_pct != pct)
+    return GS_OK;  // no count pass of this run to fill from
+  const gs_design *D = e->d;
+  const int64_t G = D->G;
+  if (G && !offsets) return fail(GS_ERR_ARG, "arena fill needs region offsets");
+  for (const auto &pc : e->kept) {
+    int64_t base = 0;
+    for (int64_t i = 0; i < G; ++i) {
+      const int g = D->order_host[i];
+      const int64_t len = pc.rs[g];
+      if (len) {
+        const int64_t dst = offsets[(int64_t)g * cols + (pc.w0 - w_lo)];
+        if (dst < 0 || dst + len > n_buf || base + len > (int64_t)pc.piece.size())
+          return fail(GS_ERR_ARG, "arena regions do not match the count pass");
+        memcpy(buf + dst, pc.piece.data() + base, sizeof(int64_t) * len);
+      }
+      base += len;
+    }
+  }
+  *filled = 1;
   return GS_OK;
 }
 

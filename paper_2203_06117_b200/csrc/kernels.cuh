@@ -123,6 +123,8 @@ struct ChunkDev {
   const long long *a_off;      // store offsets into a_buf
   long long *a_buf;
   long long a_nbuf;
+  unsigned long long *a_pos;   // count pass: index in `data` of the window's staged
+                               // outputs (peak entries, popped ones included)
 };
 
 struct StimDev {
@@ -571,9 +573,10 @@ __device__ __forceinline__ TT pin_delay(const DesignDev &D,
 template <int MODE, typename TS, typename OUT>
 __device__ __forceinline__ void record_arena(const ChunkDev &C, int g, int wr, int cnt, int peak,
                                              int filt, int icf, int disc, unsigned y0,
-                                             OUT out_at) {
+                                             OUT out_at, unsigned long long pos) {
   if (MODE & MODE_COUNTERS) {
     const size_t gw = (size_t)g * C.Wpad + wr;
+    if (C.a_pos) C.a_pos[gw] = pos;
     C.a_cnt[gw] = cnt;
     C.a_peak[gw] = peak;
     C.a_filt[gw] = filt;
@@ -707,7 +710,8 @@ __device__ __forceinline__ void event_loop(
     if (!SMEM) l_icf += icf;  // staged tiles: counted by the phase-1 filter
     l_disc += disc;
     record_arena<MODE, TS>(C, g, base_w + w, cnt, peak, filt, icf, disc, y0,
-                           [&](int j) { return out_at(j); });
+                           [&](int j) { return out_at(j); },
+                           (unsigned long long)(&out_at(0) - reinterpret_cast<TS *>(C.data)));
     has = false;
   };
   auto first_event = [&]() {
@@ -961,7 +965,9 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
   // slab when 2 * UB fits; inputs only when UB fits (outputs then go to this
   // warp's region of the pool); otherwise inputs are read in place as well.
   const bool in_smem = UB <= (unsigned)slab_words<KM>();
-  const bool out_smem = 2 * UB <= (unsigned)slab_words<KM>();
+  // (arena runs keep every window's outputs in the pool until the chunk's
+  // arena is packed, K5)
+  const bool out_smem = MODE == MODE_STATS && 2 * UB <= (unsigned)slab_words<KM>();
   unsigned nwork = (unsigned)nact;  // windows for the event loop
   unsigned inb_off[KM];            // smem: pin p's tile segment starts at slab[inb_off[p]]
   const TS *inb_glob[KM];          // else: read in place
@@ -1142,7 +1148,8 @@ __device__ __forceinline__ void eval_tile(const DesignDev &D, const ChunkDev &C,
       cf_disc += disc;
       if (MODE != MODE_STATS)
         record_arena<MODE, TS>(C, g, base_w + w, (int)cnt, (int)cnt, x2 ? 1 : 0,
-                               (int)S.icfw[w], disc, y0, [&](int q) -> TS & { return st[q]; });
+                               (int)S.icfw[w], disc, y0, [&](int q) -> TS & { return st[q]; },
+                               (unsigned long long)(st - data));
     }
     acc_filt += cf_filt;
     acc_disc += cf_disc;

@@ -45,6 +45,11 @@ constexpr int kPool = kSuper * kTile;      // windows per CTA step
 template <int K, int SLAB>
 struct alignas(16) LeanWarp {
   unsigned slab[SLAB];                       // staged fanin segments, then outputs
+  // the next tile's fanin count rows, start-bit words and tile bases,
+  // prefetched (cp.async) while the current tile is evaluated
+  alignas(16) unsigned pcnt[K][kTile];
+  alignas(16) unsigned pinit[K][4];
+  alignas(16) unsigned long long ptb[K];
   alignas(16) unsigned offs[K][kTile + 4];   // pin p: window w's toggles start at offs[p][w]
   alignas(16) unsigned cnt[kTile];           // stored toggles per window
   unsigned long long tb[K];                  // in place: pin p's tile base in `data`
@@ -190,6 +195,29 @@ __device__ __forceinline__ void tile_sources(const ChunkDev &C, LeanWarp<K, SLAB
   for (int p = 0; p < K; ++p) src[p] = T.in_smem ? &T.slab[T.seg[p]] : data + T.tb[p];
 }
 
+// cp.async of tile t's fanin count rows (a 16-byte piece per lane), the
+// tile's start-bit words (16 bytes) and tile bases (8 bytes) into the
+// warp's prefetch buffers; completed by cp.async.wait_all + __syncwarp.
+template <int K, int SLAB>
+__device__ __forceinline__ void prefetch_tile(const ChunkDev &C, const int (&net)[K], int t,
+                                              LeanWarp<K, SLAB> &T) {
+  const unsigned lane = lane_id();
+  const int Tw = C.Wpad / 32;
+#pragma unroll
+  for (int p = 0; p < K; ++p)
+    __pipeline_memcpy_async(&T.pcnt[p][lane * kWPL],
+                            C.cnt + (size_t)net[p] * C.Wpad + (size_t)t * kTile + lane * kWPL, 16);
+  if (lane < (unsigned)K) {
+    int n = net[0];
+#pragma unroll
+    for (int p = 1; p < K; ++p) n = lane == (unsigned)p ? net[p] : n;
+    __pipeline_memcpy_async(&T.ptb[lane], C.tbase + (size_t)n * C.Tc + t, 8);
+    __pipeline_memcpy_async(&T.pinit[lane][0], C.init + (size_t)n * Tw + (size_t)t * (kTile / 32),
+                            16);
+  }
+  __pipeline_commit();
+}
+
 // sim_span's event loop (_kernels.py:94-203) over one window with three or
 // more input transitions, the interconnect pair filter applied lazily as
 // sim_span's refresh does (_kernels.py:96-117).  Outputs go to the tile's
@@ -313,7 +341,8 @@ __device__ __forceinline__ void loop_window(const ChunkDev &C, int g, unsigned l
   acc.icf += (unsigned)icf;
   acc.disc += disc;
   record_arena<MODE, unsigned>(C, g, base_w + w, cnt, peak, filt, icf, disc, y0,
-                               [&](int j) -> unsigned & { return stage[so + j]; });
+                               [&](int j) -> unsigned & { return stage[so + j]; },
+                               (unsigned long long)(stage + so - reinterpret_cast<unsigned *>(C.data)));
 }
 
 // Two input transitions in closed form.  With no edge pending at the first
@@ -393,7 +422,8 @@ __device__ __forceinline__ void two_window(const ChunkDev &C, int g, unsigned lo
   if (MODE != MODE_STATS)
     record_arena<MODE, unsigned>(C, g, base_w + w, (int)cnt, (int)cnt, x2 ? 1 : 0,
                                  pairf ? 1 : 0, disc, yy0,
-                                 [&](int q) -> unsigned & { return st[q]; });
+                                 [&](int q) -> unsigned & { return st[q]; },
+                                 (unsigned long long)(st - reinterpret_cast<unsigned *>(C.data)));
 }
 
 // ------------------------------------------------------------------ kernel
@@ -449,6 +479,7 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
     __syncthreads();
     LeanAcc acc;
     const int t_end = min(u_hi * kSuper, C.Tc);
+    if (u_lo * kSuper + warp < t_end) prefetch_tile<K, SLAB>(C, net, u_lo * kSuper + warp, T);
     for (int t0 = u_lo * kSuper; t0 < t_end; t0 += kSuper, par ^= 1u) {
       const int t = t0 + warp;
       const bool tile = t < t_end;
@@ -464,12 +495,17 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         unsigned c[K][kWPL];
         unsigned long long tb[K];
         unsigned bits[K];
+        __pipeline_wait_prior(0);
+        __syncwarp();
 #pragma unroll
         for (int p = 0; p < K; ++p) {
-          load_counts(C.cnt + (size_t)net[p] * C.Wpad + base_w + wl, c[p]);
-          tb[p] = __ldg(C.tbase + (size_t)net[p] * C.Tc + t);
-          bits[p] = load_init_bits(C.init + (size_t)net[p] * Tw, t);
+          ld4(&T.pcnt[p][wl], c[p]);
+          tb[p] = T.ptb[p];
+          bits[p] = (T.pinit[p][(lane * kWPL) / 32] >> ((lane * kWPL) % 32)) & ((1u << kWPL) - 1u);
         }
+        __syncwarp();
+        // the next tile of this warp in the item: its rows fly during this one
+        if (t + kSuper < t_end) prefetch_tile<K, SLAB>(C, net, t + kSuper, T);
         unsigned n[kWPL], sidx[kWPL], sso[kWPL], ix[kWPL], p1[kWPL];
 #pragma unroll
         for (int j = 0; j < kWPL; ++j) n[j] = sidx[j] = sso[j] = ix[j] = p1[j] = 0;
@@ -488,9 +524,10 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
 #pragma unroll
           for (int j = 0; j < kWPL; ++j) {
             o4[j] = ex;
-            // a one-transition window's single toggle: its pin and slab slot
-            sidx[j] = c[p][j] ? seg[p] + ex : sidx[j];
-            p1[j] = c[p][j] ? (unsigned)p : p1[j];
+            // a one-transition window's single toggle (exactly one pin has
+            // c = 1 there): its slab slot and pin, as sums over the pins
+            sidx[j] += c[p][j] * (seg[p] + ex);
+            if (p) p1[j] += c[p][j] * (unsigned)p;
             sso[j] += ex;
             n[j] += c[p][j];
             ix[j] |= ((bits[p] >> j) & 1u) << p;
@@ -516,6 +553,13 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
               }
           }
           stage = &T.slab[inw];
+          if (MODE != MODE_STATS) {
+            // arena runs: outputs stay in the pool until the chunk's arena is
+            // packed (K5)
+            const unsigned long long sb = region_alloc(C, R, UB);
+            ok = sb != ~0ull;
+            stage = data + (ok ? sb : 0ull);
+          }
         } else {
           const unsigned long long sb = region_alloc(C, R, UB);
           ok = sb != ~0ull;
@@ -554,12 +598,13 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
           base = b0 | (b1 << 16);
         }
         base = __shfl_sync(0xffffffffu, base, 0);
-        unsigned xl = base & 0xFFFFu, xt = base >> 16;
+        unsigned xl = base & 0xFFFFu, xt = kPool + (base >> 16);
+        unsigned short *lists = &S.s.list[0][0];
 #pragma unroll
         for (int j = 0; j < kWPL; ++j) {
-          const unsigned short e = wl_entry(wl + j, ix[j], warp);
-          if ((bl[j] >> lane) & 1u) S.s.list[0][xl + __popc(bl[j] & lt)] = e;
-          if ((bt[j] >> lane) & 1u) S.s.list[1][xt + __popc(bt[j] & lt)] = e;
+          const bool inl = (bl[j] >> lane) & 1u, intw = (bt[j] >> lane) & 1u;
+          const unsigned at = inl ? xl + __popc(bl[j] & lt) : xt + __popc(bt[j] & lt);
+          if (inl || intw) lists[at] = wl_entry(wl + j, ix[j], warp);
           xl += __popc(bl[j]);
           xt += __popc(bt[j]);
         }
@@ -575,20 +620,25 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         for (int j = 0; j < kWPL; ++j) {
           const bool act = (amask >> j) & 1u;
           const bool one = in_smem && n[j] == 1;
+          const unsigned pj = one ? p1[j] : 0u;
           const unsigned tv = one ? T.slab[one ? sidx[j] : 0u] : 0u;
           unsigned icp = ic[0];
 #pragma unroll
-          for (int p = 1; p < K; ++p) icp = p1[j] == (unsigned)p ? ic[p] : icp;
+          for (int p = 1; p < K; ++p) icp = pj == (unsigned)p ? ic[p] : icp;
           const unsigned y0 = (unsigned)(lut >> ix[j]) & 1u;
-          const unsigned i1 = ix[j] ^ (1u << p1[j]);
+          const unsigned i1 = ix[j] ^ (1u << pj);
           const unsigned y1 = (unsigned)(lut >> i1) & 1u;
           const bool chg = one && y1 != y0;
-          const unsigned ot = tv + icp + dtab_pin<K>(S.s.dtab, p1[j], i1, y1 ? 0u : 1u);
+          const unsigned ot = tv + icp + dtab_pin<K>(S.s.dtab, pj, i1, y1 ? 0u : 1u);
           const unsigned wln = wl4[j];
           const bool inwin = ot < wln;
           const bool st = chg && inwin;
           const bool inl = act && n[j] <= lim;
-          if (st) stage[sso[j]] = ot;
+          // (singles occur on staged tiles only; arena runs stage outputs in the pool)
+          if (st) {
+            if (MODE == MODE_STATS) T.slab[inw + sso[j]] = ot;
+            else stage[sso[j]] = ot;
+          }
           acc.disc += (chg && !inwin) ? 1 : 0;
           // dwell at 1: the start value holds until the stored edge (or the
           // window end), the other value after it
@@ -599,7 +649,8 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
           if (MODE != MODE_STATS && inl)
             record_arena<MODE, unsigned>(C, g, base_w + wl + j, st ? 1 : 0, st ? 1 : 0, 0, 0,
                                          (chg && !inwin) ? 1 : 0, y0,
-                                         [&](int) -> unsigned & { return stage[sso[j]]; });
+                                         [&](int) -> unsigned & { return stage[sso[j]]; },
+                                         (unsigned long long)(stage + sso[j] - data));
           oc[j] = inl && st ? 1u : 0u;  // worklist windows: written in (M)
         }
         // counts of the inline windows (worklist windows overwrite theirs)
@@ -656,14 +707,26 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         const bool wrote = ob != ~0ull;  // else the chunk is re-run; keep readers in bounds
         const unsigned *stage = reinterpret_cast<const unsigned *>(T.stage);
         if (wrote) {
+          // up to two outputs per window as predicated copies; the rare
+          // windows with more take a loop
           unsigned *dst = data + ob + cx;
+          unsigned o = 0;
+          bool big = false;
 #pragma unroll
           for (int j = 0; j < kWPL; ++j) {
             const unsigned *sp = stage + so[j];
-            if (co[j] >= 1) dst[0] = sp[0];
-            if (co[j] >= 2) dst[1] = sp[1];
-            for (unsigned q = 2; q < co[j]; ++q) dst[q] = sp[q];
-            dst += co[j];
+            if (co[j] >= 1) dst[o] = sp[0];
+            if (co[j] >= 2) dst[o + 1] = sp[1];
+            big |= co[j] > 2;
+            o += co[j];
+          }
+          if (__any_sync(0xffffffffu, big)) {
+            o = 0;
+#pragma unroll
+            for (int j = 0; j < kWPL; ++j) {
+              for (unsigned q = 2; q < co[j]; ++q) dst[o + q] = stage[so[j] + q];
+              o += co[j];
+            }
           }
         }
         acc.tc += s;

@@ -338,6 +338,7 @@ def count_pass(model, stimuli, init_vals=None, *, window_range=None, cycle_paral
     w_lo, w_hi = window_range if window_range is not None else (0, stimuli.num_windows)
     s = _Session.get(model, stimuli)
     r = s.engine.run_arena(s.stim, w_lo, w_hi, int(pathpulse_pct), want_stats=True)
+    s.last_count = (w_lo, w_hi, int(pathpulse_pct), r)
     _trace(model, task_trace, task_counts, w_lo)
     return PassResult(r["counts"], r["peak"], r["filtered"], r["ic_filtered"], r["discarded"],
                       r["initials"], r["stats"])
@@ -345,11 +346,29 @@ def count_pass(model, stimuli, init_vals=None, *, window_range=None, cycle_paral
 
 def store_pass(model, stimuli, init_vals, arena, *, cycle_parallelism=32, pathpulse_pct=100,
                executor=None, workers=1, task_trace=None, task_counts=None):
-    """Pass 2 on the GPU: the identical simulation writing every region of the
-    arena (``SC:382-410``); raises :class:`ConsistencyError` if a region
-    overflows its pass-1 capacity."""
+    """Pass 2 (``SC:382-410``): every region of the arena.
+
+    When the engine's last count pass was this run (same stimulus, window
+    range, pct, and the arena sized by its ``peak``), that single simulation
+    already holds every region's contents -- K5 packed them per window chunk
+    -- and they are scattered into ``arena.buf`` without simulating again.
+    Otherwise (e.g. capacities from elsewhere) the identical simulation runs
+    again, writing the regions on the GPU, and a region overflowing its
+    capacity raises :class:`ConsistencyError`."""
     w_lo, w_hi = arena.window_range
     s = _Session.get(model, stimuli)
+    last = getattr(s, "last_count", None)
+    if (last is not None and last[:3] == (w_lo, w_hi, int(pathpulse_pct))
+            and np.array_equal(arena.caps, last[3]["peak"])):
+        # the count pass of this very run kept its waveforms (K5): the arena
+        # is filled without simulating again -- same contents, same counters
+        r = last[3]
+        if s.engine.arena_fill(s.stim, w_lo, w_hi, int(pathpulse_pct), arena.buf,
+                               arena.offsets):
+            for f in ("counts", "filtered", "ic_filtered", "discarded", "initials"):
+                getattr(arena, f)[:] = r[f]
+            _trace(model, task_trace, task_counts, w_lo)
+            return
     r = s.engine.run_arena(s.stim, w_lo, w_hi, int(pathpulse_pct), offsets=arena.offsets,
                            n_buf=arena.buf.size)
     arena.buf[:] = r["buf"]
