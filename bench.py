@@ -79,9 +79,65 @@ def host_cpu():
     return "unknown"
 
 
+class RcaConfig:
+    """the 20-bit ripple-carry adder, 1k windows, full SDF,
+    built from its text documents through the parsers (synth.rca_docs)."""
+    name = "C1"
+    description = ("small combinational netlist (20-bit ripple-carry adder, 100 gates), "
+                   "1k cycles, full SDF (COND + INTERCONNECT), text documents")
+    windows = 1000
+    pct = 100
+    averaged = False
+    ppis = 0
+
+    def __init__(self):
+        import paper_2203_06117_b200 as api
+        from paper_2203_06117_b200 import synth
+        lib_t, net_t, sdf_t, vcd_t, period = synth.rca_docs()
+        nl = api.parse_netlist(net_t, api.parse_library(lib_t))
+        lv = api.levelize(nl)
+        delays = api.parse_sdf(sdf_t, nl)
+        waves, duration = api.parse_vcd(vcd_t, nl)
+        b = api.window_boundaries(duration, period=period)
+        self.stim = api.StimulusSet.build(waves, nl, b)
+        self.model = api.compile_design(lv, delays)
+        self.period = period
+        self.gates = nl.num_gates
+        self.levels = lv.num_levels
+        self.num_inputs = nl.num_pis
+
+
+def is_rca(cfg):
+    return getattr(cfg, "name", "") == "C1"
+
+
+def design_of(cfg):
+    from paper_2203_06117_b200 import synth
+    return cfg.model if is_rca(cfg) else synth.design(cfg)
+
+
+def host_stimulus(cfg, lo, hi):
+    """Per-input CSR stimulus of windows [lo, hi) (the oracle's input)."""
+    from paper_2203_06117_b200 import synth
+    if is_rca(cfg):
+        assert (lo, hi) == (0, cfg.windows), "C1 runs its whole stimulus"
+        return cfg.stim
+    return synth.stimulus(cfg, lo, hi)
+
+
+def device_stimulus(cfg, dev, lo, hi):
+    from paper_2203_06117_b200 import _native
+    if is_rca(cfg):
+        return _native.Stimulus(dev, host_stimulus(cfg, lo, hi))
+    return _native.SynthStimulus(dev, cfg, lo, hi)
+
+
 def pick_config(args, world):
     from paper_2203_06117_b200 import synth
     name = args.config or ("C3" if world == 1 else "C4")
+    if name == "C1":
+        cfg = RcaConfig()
+        return cfg, cfg.windows
     cfg = synth.config(name)
     if args.windows:
         per_gpu = args.windows
@@ -162,12 +218,11 @@ def oracle_run(cfg, model, w_lo, w_hi, threads):
     passes and compute_stats -- the reference's path from per-input
     waveforms to per-net statistics."""
     from oracle import port
-    from paper_2203_06117_b200 import synth
     port.build()
     m = model
     d = port.Design.from_arrays(m.num_pis, m.order, m.level_starts, m.pin_off, m.pin_net,
                                 m.pin_ic, m.pin_arc, m.arc_rows, m.lut_off, m.lut_bits)
-    s = synth.stimulus(cfg, w_lo, w_hi)
+    s = host_stimulus(cfg, w_lo, w_hi)
     t0 = time.perf_counter()
     st = port.Stimulus.from_csr(s.pi_off, s.pi_times, s.pi_init, s.boundaries)
     arena = port.two_pass_simulate(d, st, pct=cfg.pct, threads=threads)
@@ -185,8 +240,8 @@ def run_reference_arm(args, rank, world):
     from paper_2203_06117_b200 import synth
     cfg, per_gpu = pick_config(args, world)
     threads = os.cpu_count() or 1
-    sample = cpu_sample_windows(args, cfg)
-    m = synth.design(cfg)
+    sample = min(cpu_sample_windows(args, cfg), per_gpu)
+    m = design_of(cfg)
     times = []
     for i in range(args.warmup + args.steps):
         lo = (i * sample) % max(1, per_gpu - sample + 1)
@@ -210,6 +265,12 @@ def run_reference_arm(args, rank, world):
                                        "extrapolates linearly (windows are independent)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def pinned_copy(a):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    return t.numpy()
 
 
 def config_desc(cfg, windows_per_gpu, world):
@@ -244,7 +305,7 @@ def main():
     os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     import torch
     import torch.distributed as dist
-    from paper_2203_06117_b200 import _native, distributed, synth
+    from paper_2203_06117_b200 import _native, distributed
 
     torch.cuda.set_device(local)
     _native.set_device(local)
@@ -252,15 +313,16 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg, per_gpu = pick_config(args, world)
     total = per_gpu * world
-    weights = _native.synth_window_counts(cfg, 0, total, local) + 1 if world > 1 else None
+    weights = (_native.synth_window_counts(cfg, 0, total, local) + 1
+               if world > 1 and not is_rca(cfg) else None)
     w_lo, w_hi = distributed.shard_windows(total, world, rank, weights)
     Wr = w_hi - w_lo
-    model = synth.design(cfg)
+    model = design_of(cfg)
     N = model.num_nets
 
     stream = torch.cuda.Stream()
     dev = model.device()
-    dstim = _native.SynthStimulus(dev, cfg, w_lo, w_hi)   # resident in HBM
+    dstim = device_stimulus(cfg, dev, w_lo, w_hi)   # resident in HBM
     eng = _native.Engine(dev, 0, stream.cuda_stream)
     acc = torch.zeros(3 * N + 3, dtype=torch.int64, device="cuda")
 
@@ -300,7 +362,12 @@ def main():
         # ---- end to end through the C ABI with host buffers: pinned host CSR
         # stimulus -> device (gs_stim_create), run, per-net sums -> host
         from paper_2203_06117_b200.waveform import StimulusSet
-        hb, hoff, htimes, hinit = dstim.download(pinned=True)
+        if is_rca(cfg):
+            hs = host_stimulus(cfg, w_lo, w_hi)
+            hb, hoff, htimes, hinit = (pinned_copy(a) for a in
+                                       (hs.boundaries, hs.pi_off, hs.pi_times, hs.pi_init))
+        else:
+            hb, hoff, htimes, hinit = dstim.download(pinned=True)
         hstim = StimulusSet.from_csr(hb, hoff, htimes, hinit)
         h2d = hb.nbytes + hoff.nbytes + htimes.nbytes + hinit.nbytes
         d2h = acc.numel() * 8

@@ -103,6 +103,9 @@ typedef struct gs_arena_out {
   const int64_t *offsets;
   int64_t *buf;
   int64_t n_buf;
+  /* store pass: region capacities [G, Ws] (pass-1 peak); a region that needs
+   * more is GS_ERR_CONSISTENCY (sim_span's cap check).  NULL: not checked. */
+  const int64_t *caps;
 } gs_arena_out;
 
 /* Timing of the last gs_run (CUDA events on the engine stream). */

@@ -54,7 +54,7 @@ class StatsOut(C.Structure):
 class ArenaOut(C.Structure):
     _fields_ = [("counts", _i64p), ("peak", _i64p), ("filtered", _i64p),
                 ("ic_filtered", _i64p), ("discarded", _i64p), ("initials", _u8p),
-                ("offsets", _i64p), ("buf", _i64p), ("n_buf", C.c_int64)]
+                ("offsets", _i64p), ("buf", _i64p), ("n_buf", C.c_int64), ("caps", _i64p)]
 
 
 class SdfDesign(C.Structure):
@@ -586,7 +586,8 @@ class Engine:
                                      C.byref(ref), C.byref(n), C.byref(g), C.byref(w)))
         return int(n.value), ((int(g.value), int(w.value)) if n.value else None)
 
-    def run_arena(self, stim, w_lo, w_hi, pct, offsets=None, n_buf=0, want_stats=False):
+    def run_arena(self, stim, w_lo, w_hi, pct, offsets=None, n_buf=0, want_stats=False,
+                  caps=None):
         """Count pass (offsets None) or store pass over [w_lo, w_hi).
 
         Returns dict of [G, Ws] arrays (counts, peak, filtered, ic_filtered,
@@ -607,6 +608,10 @@ class Engine:
             res["buf"] = buf
             a.offsets, a.buf, a.n_buf = _p64(off), (_p64(buf) if buf.size else
                                                     C.cast(C.c_void_p(8), _i64p)), buf.size
+            if caps is not None:
+                cp = _c64(caps)
+                res["_caps"] = cp
+                a.caps = _p64(cp)
         st = None
         if want_stats:
             N = self.design.num_nets

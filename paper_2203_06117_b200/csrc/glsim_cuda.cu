@@ -445,7 +445,7 @@ struct gs_engine {
   // arena workspace
   int64_t arena_windows = 0;
   long long *a_cnt = nullptr, *a_peak = nullptr, *a_filt = nullptr, *a_icf = nullptr,
-            *a_disc = nullptr, *a_off = nullptr, *a_buf = nullptr;
+            *a_disc = nullptr, *a_off = nullptr, *a_buf = nullptr, *a_capd = nullptr;
   unsigned char *a_init = nullptr;
   unsigned long long *a_pos = nullptr;
   int64_t a_buf_cap = 0;
@@ -472,6 +472,7 @@ struct gs_engine {
   void release_meta() { dfree(cnt); dfree(tbase); dfree(init); dfree(wlen32); meta_windows = 0; }
   void release_arena() {
     dfree(a_cnt); dfree(a_peak); dfree(a_filt); dfree(a_icf); dfree(a_disc); dfree(a_off);
+    dfree(a_capd);
     dfree(a_init); dfree(a_pos); arena_windows = 0;
   }
   void release() {
@@ -603,6 +604,7 @@ int ensure_arena(gs_engine *e, int64_t wins, bool store) {
   TRY(dalloc(&e->a_disc, n));
   TRY(dalloc(&e->a_init, n));
   TRY(dalloc(&e->a_off, n));
+  TRY(dalloc(&e->a_capd, n));
   TRY(dalloc(&e->a_pos, n));
   e->arena_windows = round_up(wins, kTile);
   return GS_OK;
@@ -830,12 +832,16 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
       C.a_disc = e->a_disc;
       C.a_init = e->a_init;
       C.a_off = e->a_off;
+      C.a_cap = (store && ro.arena->caps) ? e->a_capd : nullptr;
       C.a_buf = e->a_buf;
       C.a_nbuf = store ? ro.arena->n_buf : 0;
       C.a_pos = e->a_pos;
       if (store) {
         CK(cudaMemcpy2DAsync(e->a_off, Wpad * 8, ro.arena->offsets + (w - ro.w_base),
                              ro.arena_cols * 8, wc * 8, G, cudaMemcpyHostToDevice, e->st));
+        if (ro.arena->caps)
+          CK(cudaMemcpy2DAsync(e->a_capd, Wpad * 8, ro.arena->caps + (w - ro.w_base),
+                               ro.arena_cols * 8, wc * 8, G, cudaMemcpyHostToDevice, e->st));
       }
     }
     CK(cudaMemsetAsync(e->acc, 0, sizeof(long long) * ACC_ROWS * N, e->st));

@@ -121,6 +121,7 @@ struct ChunkDev {
   long long *a_cnt, *a_peak, *a_filt, *a_icf, *a_disc;
   unsigned char *a_init;
   const long long *a_off;      // store offsets into a_buf
+  const long long *a_cap;      // store: region capacities (pass-1 peak), or null
   long long *a_buf;
   long long a_nbuf;
   unsigned long long *a_pos;   // count pass: index in `data` of the window's staged
@@ -586,8 +587,9 @@ __device__ __forceinline__ void record_arena(const ChunkDev &C, int g, int wr, i
   }
   if ((MODE & MODE_STORE) == MODE_STORE) {
     const long long o = C.a_off[(size_t)g * C.Wpad + wr];
+    const long long cap = C.a_cap ? C.a_cap[(size_t)g * C.Wpad + wr] : (long long)peak;
     const long long b_lo = C.bnd[C.w0 + wr];
-    if (o >= 0 && o + peak <= C.a_nbuf) {
+    if (o >= 0 && peak <= cap && o + peak <= C.a_nbuf) {
       for (int j = 0; j < peak; ++j) C.a_buf[o + j] = (long long)out_at(j) + b_lo;
     } else if (peak) {
       atomicExch(C.err + ERR_CAP, 1);

@@ -370,7 +370,7 @@ def store_pass(model, stimuli, init_vals, arena, *, cycle_parallelism=32, pathpu
             _trace(model, task_trace, task_counts, w_lo)
             return
     r = s.engine.run_arena(s.stim, w_lo, w_hi, int(pathpulse_pct), offsets=arena.offsets,
-                           n_buf=arena.buf.size)
+                           n_buf=arena.buf.size, caps=arena.caps)
     arena.buf[:] = r["buf"]
     arena.counts[:] = r["counts"]
     arena.filtered[:] = r["filtered"]

@@ -342,3 +342,40 @@ def test_stimulus_upload_overlaps_a_running_simulation():
                 assert np.array_equal(a, b)
             assert got[3] == ref[3]
         fut.result()
+
+
+@pytest.mark.parametrize("name", ["demo_pct50", "busy_pct0", "many_windows", "rnd04"])
+def test_arena_comes_from_one_simulation(monkeypatch, name):
+    # two_pass_simulate runs the GPU simulation once: the count pass keeps
+    # every region's peak entries (K5) and the store pass only scatters them
+    # -- and the arena, transient slots of pct < 100 included, is the
+    # reference's byte for byte
+    from paper_2203_06117_b200 import _native
+    calls = []
+    real = _native.Engine.run_arena
+
+    def counting(self, *a, **k):
+        calls.append(k.get("offsets") is not None)
+        return real(self, *a, **k)
+
+    monkeypatch.setattr(_native.Engine, "run_arena", counting)
+    docs, ref = load_golden(name)
+    nl, lv, delays, stim, arena, diag, stats = gpu_run(docs)
+    assert calls and not any(calls), "a second (store) simulation ran"
+    for f in ARENA_FIELDS:
+        assert np.array_equal(getattr(arena, f), ref[f]), f"{name}: arena.{f}"
+
+
+def test_store_pass_with_foreign_capacities_simulates_and_checks():
+    # capacities that are not the count pass's own take the real store pass,
+    # which still detects a region overflowing its capacity
+    docs, ref = load_golden("many_windows")
+    nl, lv, delays, waves, duration, b, stim = gen.load(docs, api)
+    model = api.compile_design(lv, delays)
+    counted = simcore.count_pass(model, stim)
+    caps = counted.peak.copy()
+    g, w = np.argwhere(caps > 0)[0]
+    caps[g, w] -= 1
+    arena = api.allocate_arena(caps, model.order, stim.boundaries, (0, stim.num_windows), lv)
+    with pytest.raises(api.ConsistencyError):
+        simcore.store_pass(model, stim, None, arena)
