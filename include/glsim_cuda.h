@@ -346,6 +346,30 @@ int gs_vcdw_finish(gs_vcdw *w, int64_t end_time);
 int gs_vcdw_take(gs_vcdw *w, char *buf, int64_t cap, int64_t *len);
 int gs_vcdw_destroy(gs_vcdw *w);
 
+/* ---- netlist document reader (host): the format upstream of the design
+ * upload ------------------------------------------- */
+
+/* parse_netlist (pkg/src/glsim/netlist.py:190-275): the netlist JSON read
+ * straight into flat arrays for the cell library given as flat names (cell
+ * c: name, input pins pin_names[cell_pin_first[c] .. cell_pin_first[c+1]),
+ * output pin).  Nets are interned as the reference does (inputs, then gate
+ * i's output as net P + i).  GS_ERR_UNSUPPORTED for any document the
+ * reference would reject (its own reader then raises the exact error). */
+typedef struct gs_netlist gs_netlist;
+int gs_netlist_parse(const char *text, int64_t len, const char *cell_names,
+                     const int64_t *cell_name_off, int64_t num_cells, const char *pin_names,
+                     const int64_t *pin_name_off, const int64_t *cell_pin_first,
+                     const char *cell_outputs, const int64_t *cell_output_off, gs_netlist **out);
+/* counts[4] = inputs, outputs, gates, pins; bytes[5] = UTF-8 bytes of the
+ * design name, input names, output names, gate names, gate output net names */
+int gs_netlist_sizes(const gs_netlist *h, int64_t *counts, int64_t *bytes);
+/* names as byte blobs with [n+1] offsets; gate_cell [G], pin_off [G+1],
+ * pin_net [pins] (any pointer may be NULL) */
+int gs_netlist_copy(const gs_netlist *h, char *name, char *pis, int64_t *pis_off, char *pos,
+                    int64_t *pos_off, char *gates, int64_t *gates_off, char *outs,
+                    int64_t *outs_off, int64_t *gate_cell, int64_t *pin_off, int64_t *pin_net);
+int gs_netlist_destroy(gs_netlist *h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -138,6 +138,13 @@ SIGNATURES = {
     "gs_vcdw_finish": (C.c_int, [C.c_void_p, C.c_int64]),
     "gs_vcdw_take": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, _i64p]),
     "gs_vcdw_destroy": (C.c_int, [C.c_void_p]),
+    "gs_netlist_parse": (C.c_int, [C.c_char_p, C.c_int64, C.c_char_p, _i64p, C.c_int64,
+                                   C.c_char_p, _i64p, _i64p, C.c_char_p, _i64p,
+                                   C.POINTER(C.c_void_p)]),
+    "gs_netlist_sizes": (C.c_int, [C.c_void_p, _i64p, _i64p]),
+    "gs_netlist_copy": (C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p, _i64p, C.c_char_p, _i64p,
+                                  C.c_char_p, _i64p, C.c_char_p, _i64p, _i64p, _i64p, _i64p]),
+    "gs_netlist_destroy": (C.c_int, [C.c_void_p]),
     "gs_saif_format": (C.c_int, [C.c_char_p, _i64p, C.c_int64, _i64p, _i64p, _i64p, _i64p,
                                  C.c_int64, C.c_char_p, C.c_char_p, C.c_int, C.c_char_p,
                                  C.c_int64, _i64p]),
@@ -219,6 +226,68 @@ def vcd_parse(text, pi_names, path=None):
     return pi_off, pi_times, pi_init, int(dur.value)
 
 
+def _names(blob, off):
+    """UTF-8 blob + byte offsets -> list of str."""
+    if not off.size or off[-1] == 0:
+        return [""] * (off.size - 1)
+    raw = bytes(blob)
+    if raw.isascii() and b"\0" not in raw:
+        # one split at C speed: a separator at every boundary
+        sep = np.frombuffer(raw, dtype=np.uint8)
+        parts = np.insert(sep, off[1:-1], 0).tobytes()
+        return parts.decode("ascii").split("\0")
+    return [raw[off[i]:off[i + 1]].decode("utf-8", errors="surrogatepass")
+            for i in range(off.size - 1)]
+
+
+def netlist_parse(text, lib):
+    """Native netlist reader (``gs_netlist_parse``): -> dict of the design
+    name, name lists and flat arrays (gate_cell, pin_off, pin_net), or None
+    when the library is not built or the document is outside the reader's
+    scope (every document the reference rejects: the Python reader then
+    raises its exact error)."""
+    try:
+        lib_ = load()
+    except RuntimeError:
+        return None
+    try:
+        raw = text.encode("utf-8") if isinstance(text, str) else bytes(text)
+    except UnicodeEncodeError:
+        return None
+    cells = list(lib.cells.values())
+    cn, cno = _blob(c.name for c in cells)
+    pn, pno = _blob(p for c in cells for p in c.input_pins)
+    first = np.zeros(len(cells) + 1, dtype=np.int64)
+    np.cumsum([len(c.input_pins) for c in cells], out=first[1:])
+    co, coo = _blob(c.output_pin for c in cells)
+    h = C.c_void_p()
+    rc = lib_.gs_netlist_parse(raw, len(raw), cn, _p64(cno), len(cells), pn, _p64(pno),
+                               _p64(first), co, _p64(coo), C.byref(h))
+    if rc == GS_ERR_UNSUPPORTED:
+        return None
+    _check(rc)
+    try:
+        cnt = np.zeros(4, dtype=np.int64)
+        nb = np.zeros(5, dtype=np.int64)
+        _check(lib_.gs_netlist_sizes(h, _p64(cnt), _p64(nb)))
+        P, O, G, NP = (int(x) for x in cnt)
+        bufs = [C.create_string_buffer(max(1, int(b))) for b in nb]
+        offs = [np.zeros(n + 1, dtype=np.int64) for n in (P, O, G, G)]
+        gate_cell = np.zeros(G, dtype=np.int64)
+        pin_off = np.zeros(G + 1, dtype=np.int64)
+        pin_net = np.zeros(NP, dtype=np.int64)
+        _check(lib_.gs_netlist_copy(h, bufs[0], bufs[1], _p64(offs[0]), bufs[2], _p64(offs[1]),
+                                    bufs[3], _p64(offs[2]), bufs[4], _p64(offs[3]),
+                                    _p64(gate_cell), _p64(pin_off), _p64(pin_net)))
+    finally:
+        lib_.gs_netlist_destroy(h)
+    name = bufs[0].raw[:int(nb[0])].decode("utf-8", errors="surrogatepass")
+    pis, pos, gates, outs = (_names(bufs[i + 1].raw[:int(nb[i + 1])], offs[i])
+                             for i in range(4))
+    return {"name": name, "pis": pis, "pos": pos, "gates": gates, "outs": outs,
+            "cells": cells, "gate_cell": gate_cell, "pin_off": pin_off, "pin_net": pin_net}
+
+
 def _blob(strings):
     """ASCII/UTF-8 strings -> (bytes, int64 byte offsets [n+1])."""
     strings = list(strings)
@@ -240,29 +309,18 @@ def _sdf_context(netlist):
     ctx = getattr(netlist, "_gs_sdf_ctx", None)
     if ctx is not None:
         return ctx
-    gates = netlist.gates
-    cells, cell_ix = [], {}
-    gate_cell = np.empty(len(gates), dtype=np.int64)
-    for i, g in enumerate(gates):
-        c = cell_ix.get(id(g.cell))
-        if c is None:
-            c = cell_ix[id(g.cell)] = len(cells)
-            cells.append(g.cell)
-        gate_cell[i] = c
-    k = np.fromiter((len(g.pin_nets) for g in gates), dtype=np.int64, count=len(gates))
-    pin_off = np.zeros(len(gates) + 1, dtype=np.int64)
-    np.cumsum(k, out=pin_off[1:])
-    pin_net = np.fromiter((n for g in gates for n in g.pin_nets), dtype=np.int64,
-                          count=int(pin_off[-1]))
-    out_net = np.fromiter((g.out_net for g in gates), dtype=np.int64, count=len(gates))
+    cells, gate_cell = netlist.cell_arrays()
+    pin_off, pin_net = netlist.pin_arrays()
+    G = gate_cell.size
+    out_net = np.arange(netlist.num_pis, netlist.num_pis + G, dtype=np.int64)
     pins = [p for c in cells for p in c.input_pins]
     first = np.zeros(len(cells) + 1, dtype=np.int64)
     np.cumsum([len(c.input_pins) for c in cells], out=first[1:])
-    keep = {"gn": _blob(g.name for g in gates), "nn": _blob(netlist.net_names),
+    keep = {"gn": _blob(netlist.gate_names), "nn": _blob(netlist.net_names),
             "pn": _blob(pins), "co": _blob(c.output_pin for c in cells),
             "first": first, "gate_cell": gate_cell, "pin_off": pin_off, "pin_net": pin_net,
             "out_net": out_net}
-    d = SdfDesign(num_gates=len(gates), num_nets=len(netlist.net_names), num_cells=len(cells))
+    d = SdfDesign(num_gates=G, num_nets=len(netlist.net_names), num_cells=len(cells))
     d.gate_names, d.gate_name_off = keep["gn"][0], _p64(keep["gn"][1])
     d.net_names, d.net_name_off = keep["nn"][0], _p64(keep["nn"][1])
     d.pin_names, d.pin_name_off = keep["pn"][0], _p64(keep["pn"][1])

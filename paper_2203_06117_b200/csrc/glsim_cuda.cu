@@ -19,6 +19,7 @@
 #include "arena.cuh"
 #include "vcd_reader.h"
 #include "vcd_writer.h"
+#include "netlist_reader.h"
 #include "sdf_reader.h"
 
 using namespace gs;
@@ -1836,6 +1837,103 @@ int gs_vcdw_take(gs_vcdw *w, char *buf, int64_t cap, int64_t *len) {
 
 int gs_vcdw_destroy(gs_vcdw *w) {
   delete w;
+  return GS_OK;
+}
+
+}  // extern "C"
+
+// =========================================================================
+// netlist JSON reader (netlist.py:190-275)
+
+struct gs_netlist {
+  gsnl::Result r;
+};
+
+namespace {
+void join_names(const std::vector<std::string> &v, std::string &blob, std::vector<int64_t> &off) {
+  off.assign(1, 0);
+  for (const auto &x : v) {
+    blob += x;
+    off.push_back((int64_t)blob.size());
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int gs_netlist_parse(const char *text, int64_t len, const char *cell_names,
+                     const int64_t *cell_name_off, int64_t num_cells, const char *pin_names,
+                     const int64_t *pin_name_off, const int64_t *cell_pin_first,
+                     const char *cell_outputs, const int64_t *cell_output_off, gs_netlist **out) {
+  if (!out || (len && !text) || num_cells < 0 ||
+      (num_cells && (!cell_names || !cell_name_off || !cell_pin_first || !cell_outputs ||
+                     !cell_output_off)))
+    return fail(GS_ERR_ARG, "bad netlist reader arguments");
+  *out = nullptr;
+  std::vector<gsnl::Cell> cells((size_t)num_cells);
+  for (int64_t c = 0; c < num_cells; ++c) {
+    cells[c].name.assign(cell_names + cell_name_off[c], cell_name_off[c + 1] - cell_name_off[c]);
+    cells[c].out.assign(cell_outputs + cell_output_off[c],
+                        cell_output_off[c + 1] - cell_output_off[c]);
+    for (int64_t q = cell_pin_first[c]; q < cell_pin_first[c + 1]; ++q)
+      cells[c].pins.emplace_back(pin_names + pin_name_off[q], pin_name_off[q + 1] - pin_name_off[q]);
+  }
+  gs_netlist *h = new gs_netlist();
+  if (!gsnl::read(text, (size_t)len, cells, h->r)) {
+    delete h;
+    return fail(GS_ERR_UNSUPPORTED, "netlist document outside the native reader's scope");
+  }
+  *out = h;
+  return GS_OK;
+}
+
+int gs_netlist_sizes(const gs_netlist *h, int64_t *counts, int64_t *bytes) {
+  if (!h || !counts || !bytes) return fail(GS_ERR_ARG, "bad netlist size arguments");
+  const gsnl::Result &r = h->r;
+  counts[0] = (int64_t)r.pis.size();
+  counts[1] = (int64_t)r.pos.size();
+  counts[2] = (int64_t)r.gates.size();
+  counts[3] = (int64_t)r.pin_net.size();
+  auto sz = [](const std::vector<std::string> &v) {
+    int64_t n = 0;
+    for (const auto &x : v) n += (int64_t)x.size();
+    return n;
+  };
+  bytes[0] = (int64_t)r.name.size();
+  bytes[1] = sz(r.pis);
+  bytes[2] = sz(r.pos);
+  bytes[3] = sz(r.gates);
+  bytes[4] = sz(r.out_names);
+  return GS_OK;
+}
+
+int gs_netlist_copy(const gs_netlist *h, char *name, char *pis, int64_t *pis_off, char *pos,
+                    int64_t *pos_off, char *gates, int64_t *gates_off, char *outs,
+                    int64_t *outs_off, int64_t *gate_cell, int64_t *pin_off, int64_t *pin_net) {
+  if (!h) return fail(GS_ERR_ARG, "null netlist");
+  const gsnl::Result &r = h->r;
+  std::string blob;
+  std::vector<int64_t> off;
+  struct { const std::vector<std::string> *v; char *b; int64_t *o; } lists[] = {
+      {&r.pis, pis, pis_off}, {&r.pos, pos, pos_off}, {&r.gates, gates, gates_off},
+      {&r.out_names, outs, outs_off}};
+  for (auto &L : lists) {
+    blob.clear();
+    join_names(*L.v, blob, off);
+    if (L.b && !blob.empty()) memcpy(L.b, blob.data(), blob.size());
+    if (L.o) memcpy(L.o, off.data(), sizeof(int64_t) * off.size());
+  }
+  if (name && !r.name.empty()) memcpy(name, r.name.data(), r.name.size());
+  if (gate_cell && !r.gate_cell.empty())
+    memcpy(gate_cell, r.gate_cell.data(), sizeof(int64_t) * r.gate_cell.size());
+  if (pin_off) memcpy(pin_off, r.pin_off.data(), sizeof(int64_t) * r.pin_off.size());
+  if (pin_net && !r.pin_net.empty())
+    memcpy(pin_net, r.pin_net.data(), sizeof(int64_t) * r.pin_net.size());
+  return GS_OK;
+}
+
+int gs_netlist_destroy(gs_netlist *h) {
+  delete h;
   return GS_OK;
 }
 

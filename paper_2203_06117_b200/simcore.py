@@ -177,31 +177,32 @@ class CompiledDesign:
             raise ValueError("delay annotation was built for a different netlist")
         self.levelized = levelized
         self.netlist = nl
-        G = nl.num_gates
-        k = np.fromiter((g.cell.num_inputs for g in nl.gates), dtype=np.int64, count=G)
-        pin_off = np.zeros(G + 1, dtype=np.int64)
-        np.cumsum(k, out=pin_off[1:])
-        cells, lut_parts, cell_off, lut_off = {}, [], 0, np.zeros(G, dtype=np.int64)
-        for gi, g in enumerate(nl.gates):
-            key = (g.cell.name, np.asarray(g.cell.truth, dtype=np.uint8).tobytes())
-            c = cells.get(key)
-            if c is None:
-                c = cells[key] = cell_off
-                lut_parts.append(np.asarray(g.cell.truth, dtype=np.uint8))
-                cell_off += len(g.cell.truth)
-            lut_off[gi] = c
-        n_pins = int(pin_off[-1])
-        pin_net = np.fromiter((n for g in nl.gates for n in g.pin_nets), dtype=np.int64,
-                              count=n_pins)
-        pin_ic = (np.concatenate([np.asarray(a, dtype=np.int64) for a in delays.interconnect])
-                  if G else np.zeros(0, dtype=np.int64))
-        tables = [t for per_gate in delays.tables for t in per_gate]
-        arc_rows = (np.concatenate(tables).astype(np.int64) if tables
-                    else np.zeros((0, 2), dtype=np.int64))
-        rows = np.repeat(np.left_shift(1, k - 1), k) if G else np.zeros(0, dtype=np.int64)
+        # array-native: the netlist's pin and cell arrays and the delays'
+        # flat tables (no per-gate Python objects on this path)
+        pin_off, pin_net = nl.pin_arrays()
+        cells, gate_cell = nl.cell_arrays()
+        # one truth table per distinct (name, truth) cell, in order of first use
+        first_use = np.full(len(cells), -1, dtype=np.int64)
+        if gate_cell.size:
+            u, at = np.unique(gate_cell, return_index=True)
+            first_use[u] = at
+        keys, lut_parts, cell_lut, top = {}, [], np.zeros(len(cells), dtype=np.int64), 0
+        for c in sorted(range(len(cells)), key=lambda c: (first_use[c] < 0, first_use[c])):
+            cell = cells[c]
+            truth = np.asarray(cell.truth, dtype=np.uint8)
+            key = (cell.name, truth.tobytes())
+            if key not in keys:
+                keys[key] = top
+                lut_parts.append(truth)
+                top += truth.size
+            cell_lut[c] = keys[key]
+        lut_off = cell_lut[gate_cell] if gate_cell.size else np.zeros(0, dtype=np.int64)
+        arc_rows, pin_ic = delays.arrays()
+        k = np.diff(pin_off)
+        rows = np.repeat(np.left_shift(np.int64(1), k - 1), k) if k.size else np.zeros(0, np.int64)
         pin_arc = np.cumsum(rows) - rows
-        self._set(levelized.order, levelized.level_starts, nl.num_pis, pin_off, pin_net,
-                  pin_ic, pin_arc, arc_rows,
+        self._set(levelized.order, levelized.level_starts, nl.num_pis, pin_off.copy(),
+                  pin_net.copy(), pin_ic.copy(), pin_arc, arc_rows.copy(),
                   lut_off, np.concatenate(lut_parts) if lut_parts else np.zeros(0, np.uint8))
 
     def _set(self, order, level_starts, num_pis, pin_off, pin_net, pin_ic, pin_arc, arc_rows,
