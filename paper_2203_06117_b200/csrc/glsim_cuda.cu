@@ -1849,15 +1849,6 @@ struct gs_netlist {
   gsnl::Result r;
 };
 
-namespace {
-void join_names(const std::vector<std::string> &v, std::string &blob, std::vector<int64_t> &off) {
-  off.assign(1, 0);
-  for (const auto &x : v) {
-    blob += x;
-    off.push_back((int64_t)blob.size());
-  }
-}
-}  // namespace
 
 extern "C" {
 
@@ -1894,16 +1885,11 @@ int gs_netlist_sizes(const gs_netlist *h, int64_t *counts, int64_t *bytes) {
   counts[1] = (int64_t)r.pos.size();
   counts[2] = (int64_t)r.gates.size();
   counts[3] = (int64_t)r.pin_net.size();
-  auto sz = [](const std::vector<std::string> &v) {
-    int64_t n = 0;
-    for (const auto &x : v) n += (int64_t)x.size();
-    return n;
-  };
   bytes[0] = (int64_t)r.name.size();
-  bytes[1] = sz(r.pis);
-  bytes[2] = sz(r.pos);
-  bytes[3] = sz(r.gates);
-  bytes[4] = sz(r.out_names);
+  bytes[1] = (int64_t)r.pis.blob.size();
+  bytes[2] = (int64_t)r.pos.blob.size();
+  bytes[3] = (int64_t)r.gates.blob.size();
+  bytes[4] = (int64_t)r.outs.blob.size();
   return GS_OK;
 }
 
@@ -1912,16 +1898,12 @@ int gs_netlist_copy(const gs_netlist *h, char *name, char *pis, int64_t *pis_off
                     int64_t *outs_off, int64_t *gate_cell, int64_t *pin_off, int64_t *pin_net) {
   if (!h) return fail(GS_ERR_ARG, "null netlist");
   const gsnl::Result &r = h->r;
-  std::string blob;
-  std::vector<int64_t> off;
-  struct { const std::vector<std::string> *v; char *b; int64_t *o; } lists[] = {
+  struct { const gsnl::Names *v; char *b; int64_t *o; } lists[] = {
       {&r.pis, pis, pis_off}, {&r.pos, pos, pos_off}, {&r.gates, gates, gates_off},
-      {&r.out_names, outs, outs_off}};
+      {&r.outs, outs, outs_off}};
   for (auto &L : lists) {
-    blob.clear();
-    join_names(*L.v, blob, off);
-    if (L.b && !blob.empty()) memcpy(L.b, blob.data(), blob.size());
-    if (L.o) memcpy(L.o, off.data(), sizeof(int64_t) * off.size());
+    if (L.b && !L.v->blob.empty()) memcpy(L.b, L.v->blob.data(), L.v->blob.size());
+    if (L.o) memcpy(L.o, L.v->off.data(), sizeof(int64_t) * L.v->off.size());
   }
   if (name && !r.name.empty()) memcpy(name, r.name.data(), r.name.size());
   if (gate_cell && !r.gate_cell.empty())

@@ -17,6 +17,7 @@
 #pragma once
 #include <cstdint>
 #include <cstring>
+#include <deque>
 #include <string>
 #include <string_view>
 #include <unordered_map>
@@ -30,13 +31,23 @@ struct Cell {
   std::string out;
 };
 
+// a list of names as one byte blob with [n+1] offsets
+struct Names {
+  std::string blob;
+  std::vector<int64_t> off{0};
+  void add(std::string_view s) {
+    blob.append(s.data(), s.size());
+    off.push_back((int64_t)blob.size());
+  }
+  size_t size() const { return off.size() - 1; }
+};
+
 struct Result {
   std::string name;
-  std::vector<std::string> pis, pos, gates;
+  Names pis, pos, gates, outs;      // outs: gate output net names
   std::vector<int64_t> gate_cell;   // [G] index into the cell list
   std::vector<int64_t> pin_off;     // [G+1]
   std::vector<int64_t> pin_net;     // [sum k], cell pin order
-  std::vector<std::string> out_names;  // [G] output net names
 };
 
 // ---------------------------------------------------------------- JSON
@@ -78,7 +89,25 @@ class Parser {
     return p_ < end_ && *p_ == '"' && str(k);
   }
   bool one(Value &v) { ws(); return value(v, 0); }
-  bool skip() { Value v; ws(); return skip_value(0); }
+  bool skip() { ws(); return skip_value(0); }
+  // a string value as a view into the text when it has no escapes, else
+  // decoded into `arena` (stable storage); false if not a valid string
+  bool fstr(std::string_view &out, std::deque<std::string> &arena) {
+    ws();
+    if (p_ >= end_ || *p_ != '"') return false;
+    const char *b = p_ + 1, *q = b;
+    while (q < end_ && *q != '"' && *q != '\\' && (unsigned char)*q >= 0x20) ++q;
+    if (q < end_ && *q == '"') {
+      out = std::string_view(b, (size_t)(q - b));
+      p_ = q + 1;
+      return true;
+    }
+    arena.emplace_back();
+    if (!str(arena.back())) return false;
+    out = arena.back();
+    return true;
+  }
+  bool peek(char c) { ws(); return p_ < end_ && *p_ == c; }
 
  private:
   const char *p_, *end_;
@@ -86,7 +115,7 @@ class Parser {
   bool skip_value(int depth) {
     if (depth > 200 || p_ >= end_) return false;
     const char c = *p_;
-    if (c == '"') { std::string t; return str(t); }
+    if (c == '"') { std::string_view v; return skip_str(); }
     if (c == '{' || c == '[') {
       const char close = c == '{' ? '}' : ']';
       ++p_;
@@ -95,8 +124,7 @@ class Parser {
       while (true) {
         ws();
         if (c == '{') {
-          std::string k;
-          if (p_ >= end_ || *p_ != '"' || !str(k)) return false;
+          if (p_ >= end_ || *p_ != '"' || !skip_str()) return false;
           ws();
           if (p_ >= end_ || *p_ != ':') return false;
           ++p_;
@@ -114,6 +142,17 @@ class Parser {
   }
   void ws() {
     while (p_ < end_ && (*p_ == ' ' || *p_ == '\t' || *p_ == '\n' || *p_ == '\r')) ++p_;
+  }
+  // a string checked without building it (escapes validated)
+  bool skip_str() {
+    const char *q = p_ + 1;
+    while (q < end_ && *q != '"' && *q != '\\' && (unsigned char)*q >= 0x20) ++q;
+    if (q < end_ && *q == '"') {
+      p_ = q + 1;
+      return true;
+    }
+    std::string t;
+    return str(t);
   }
   bool lit(const char *w) {
     const size_t n = strlen(w);
@@ -276,10 +315,77 @@ class Parser {
 };
 
 // ---------------------------------------------------------------- netlist
+// open-addressing string_view -> int64 map (linear probing, power-of-two
+// capacity): the name tables of a multi-million-gate netlist, without a heap
+// node per entry
+class NameMap {
+ public:
+  explicit NameMap(size_t expect = 16) { grow(expect * 2); }
+  // inserts (key, v) unless present; returns false if the key was present
+  bool insert(std::string_view k, int64_t v) {
+    if ((n_ + 1) * 4 > cap_ * 3) grow(cap_ * 2);
+    size_t i = slot(k);
+    if (used_[i]) return false;
+    used_[i] = 1;
+    keys_[i] = k;
+    vals_[i] = v;
+    ++n_;
+    return true;
+  }
+  // value of k, or -1
+  int64_t find(std::string_view k) const {
+    const size_t i = slot(k);
+    return used_[i] ? vals_[i] : -1;
+  }
+
+ private:
+  std::vector<std::string_view> keys_;
+  std::vector<int64_t> vals_;
+  std::vector<char> used_;
+  size_t cap_ = 0, n_ = 0;
+  static uint64_t hash(std::string_view k) {
+    uint64_t h = 1469598103934665603ull;  // FNV-1a, then a final mix
+    for (unsigned char c : k) h = (h ^ c) * 1099511628211ull;
+    h ^= h >> 33;
+    h *= 0xff51afd7ed558ccdull;
+    h ^= h >> 33;
+    return h;
+  }
+  size_t slot(std::string_view k) const {
+    size_t i = (size_t)hash(k) & (cap_ - 1);
+    while (used_[i] && keys_[i] != k) i = (i + 1) & (cap_ - 1);
+    return i;
+  }
+  void grow(size_t want) {
+    size_t c = 16;
+    while (c < want) c <<= 1;
+    std::vector<std::string_view> ok;
+    std::vector<int64_t> ov;
+    for (size_t i = 0; i < cap_; ++i)
+      if (used_[i]) {
+        ok.push_back(keys_[i]);
+        ov.push_back(vals_[i]);
+      }
+    cap_ = c;
+    keys_.assign(c, std::string_view());
+    vals_.assign(c, 0);
+    used_.assign(c, 0);
+    n_ = 0;
+    for (size_t i = 0; i < ok.size(); ++i) {
+      const size_t j = slot(ok[i]);
+      used_[j] = 1;
+      keys_[j] = ok[i];
+      vals_[j] = ov[i];
+      ++n_;
+    }
+  }
+};
+
 // false: the document is outside the reader's scope (the caller's reader
 // then produces the reference's result or error).  Two passes: the top-level
 // object is scanned for the (last) "name", "inputs", "outputs" and "gates"
-// values; then the gates array is streamed one entry at a time.
+// values; then the gates array is streamed one entry at a time, strings held
+// as views into the text (decoded copies only where they carry escapes).
 inline bool read(const char *text, size_t len, const std::vector<Cell> &cells, Result &R) {
   Parser top(text, len);
   const char *at[4] = {nullptr, nullptr, nullptr, nullptr};  // name, inputs, outputs, gates
@@ -289,7 +395,7 @@ inline bool read(const char *text, size_t len, const std::vector<Cell> &cells, R
     while (true) {
       std::string k;
       if (!top.key(k) || !top.eat(':')) return false;
-      top.eat(' ');  // (whitespace is skipped by the next call anyway)
+      top.peek(' ');
       const char *v = top.pos();
       for (int i = 0; i < 4; ++i)
         if (k == keys[i]) at[i] = v;
@@ -300,71 +406,117 @@ inline bool read(const char *text, size_t len, const std::vector<Cell> &cells, R
     }
   }
   if (!top.at_end()) return false;
-  auto parse_at = [&](const char *p, Value &v) {
-    Parser q(p, (size_t)(text + len - p));
-    return q.one(v);
-  };
-  Value name, ins, outs;
-  if (!at[0] || !parse_at(at[0], name) || name.kind != Value::STR || name.s.empty()) return false;
-  R.name = name.s;
-  auto str_list = [&](const char *p, std::vector<std::string> &out, Value &tmp) {
+  std::deque<std::string> arena;  // decoded strings (escapes); views point here
+  auto cursor = [&](const char *p) { return Parser(p, (size_t)(text + len - p)); };
+  {
+    if (!at[0]) return false;
+    Parser q = cursor(at[0]);
+    std::string_view nm;
+    if (!q.fstr(nm, arena) || nm.empty()) return false;
+    R.name.assign(nm.data(), nm.size());
+  }
+  auto str_list = [&](const char *p, Names &out) {
     if (!p) return true;  // absent: empty
-    if (!parse_at(p, tmp) || tmp.kind != Value::ARR) return false;
-    for (auto &x : tmp.arr) {
-      if (x.kind != Value::STR) return false;
-      out.push_back(std::move(x.s));
+    Parser q = cursor(p);
+    if (!q.eat('[')) return false;
+    if (q.eat(']')) return true;
+    while (true) {
+      std::string_view v;
+      if (!q.fstr(v, arena)) return false;
+      out.add(v);
+      if (q.eat(',')) continue;
+      return q.eat(']');
     }
-    return true;
   };
-  if (!str_list(at[1], R.pis, ins) || !str_list(at[2], R.pos, outs)) return false;
+  if (!str_list(at[1], R.pis) || !str_list(at[2], R.pos)) return false;
 
-  std::unordered_map<std::string, int64_t> cell_ix, net_ix;
-  for (size_t c = 0; c < cells.size(); ++c) cell_ix.emplace(cells[c].name, (int64_t)c);
+  NameMap cell_ix(cells.size()), net_ix((size_t)(len / 48) + R.pis.size()),
+      seen((size_t)(len / 96));
+  for (size_t c = 0; c < cells.size(); ++c) cell_ix.insert(cells[c].name, (int64_t)c);
   int64_t nets = 0;
-  for (const auto &pi : R.pis)
-    if (!net_ix.emplace(pi, nets++).second) return false;  // two drivers
-  std::unordered_map<std::string, char> seen;
-  std::vector<std::string> pending;  // pin nets not yet driven when read
+  for (size_t i = 0; i < R.pis.size(); ++i)
+    if (!net_ix.insert(std::string_view(R.pis.blob).substr(R.pis.off[i],
+                                                          R.pis.off[i + 1] - R.pis.off[i]),
+                       nets++))
+      return false;  // two drivers
+  std::vector<std::string_view> pending;  // pin nets not yet driven when read
   R.pin_off.assign(1, 0);
+  std::vector<std::pair<std::string_view, std::string_view>> pins;
   if (at[3]) {
-    Parser gp(at[3], (size_t)(text + len - at[3]));
+    Parser gp = cursor(at[3]);
     if (!gp.eat('[')) return false;
     if (!gp.eat(']')) {
       while (true) {
-        Value e;
-        if (!gp.one(e) || e.kind != Value::OBJ) return false;
-        const Value *gn = e.get("name"), *cn = e.get("cell"), *pins = e.get("pins");
-        if (!gn || gn->kind != Value::STR || gn->s.empty()) return false;
-        if (!seen.emplace(gn->s, 1).second) return false;  // duplicate gate name
-        if (!cn || cn->kind != Value::STR) return false;
-        auto ci = cell_ix.find(cn->s);
-        if (ci == cell_ix.end()) return false;
-        if (!pins || pins->kind != Value::OBJ) return false;
-        const Cell &cell = cells[ci->second];
-        for (const auto &kv : pins->obj) {
-          if (kv.second.kind != Value::STR) return false;
+        // one gate entry: {"name": str, "cell": str, "pins": {str: str}}
+        std::string_view gn, cn;
+        bool have_gn = false, have_cn = false, have_pins = false;
+        if (!gp.eat('{')) return false;
+        if (!gp.eat('}')) {
+          while (true) {
+            std::string_view k;
+            if (!gp.fstr(k, arena) || !gp.eat(':')) return false;
+            if (k == "name") {
+              if (!gp.fstr(gn, arena)) return false;
+              have_gn = true;
+            } else if (k == "cell") {
+              if (!gp.fstr(cn, arena)) return false;
+              have_cn = true;
+            } else if (k == "pins") {
+              pins.clear();
+              have_pins = true;
+              if (!gp.eat('{')) return false;
+              if (!gp.eat('}')) {
+                while (true) {
+                  std::string_view pk, pv;
+                  if (!gp.fstr(pk, arena) || !gp.eat(':') || !gp.fstr(pv, arena)) return false;
+                  pins.emplace_back(pk, pv);
+                  if (gp.eat(',')) continue;
+                  if (gp.eat('}')) break;
+                  return false;
+                }
+              }
+            } else if (!gp.skip()) {
+              return false;
+            }
+            if (gp.eat(',')) continue;
+            if (gp.eat('}')) break;
+            return false;
+          }
+        }
+        if (!have_gn || gn.empty() || !have_cn || !have_pins) return false;
+        if (!seen.insert(gn, 1)) return false;  // duplicate gate name
+        const int64_t ci = cell_ix.find(cn);
+        if (ci < 0) return false;
+        const Cell &cell = cells[ci];
+        auto last = [&](std::string_view key) -> const std::string_view * {
+          const std::string_view *v = nullptr;
+          for (const auto &kv : pins)
+            if (kv.first == key) v = &kv.second;
+          return v;
+        };
+        for (const auto &kv : pins) {
           bool legal = kv.first == cell.out;
           for (const auto &p : cell.pins) legal |= kv.first == p;
           if (!legal) return false;
         }
-        const Value *ov = pins->get(cell.out);
+        const std::string_view *ov = last(cell.out);
         if (!ov) return false;
         for (const auto &p : cell.pins) {
-          const Value *src = pins->get(p);
+          const std::string_view *src = last(p);
           if (!src) return false;
-          auto it = net_ix.find(src->s);
-          if (it != net_ix.end()) {
-            R.pin_net.push_back(it->second);
+          const int64_t nx = net_ix.find(*src);
+          if (nx >= 0) {
+            R.pin_net.push_back(nx);
           } else {  // resolved once every output is claimed
             R.pin_net.push_back(-1 - (int64_t)pending.size());
-            pending.push_back(src->s);
+            pending.push_back(*src);
           }
         }
-        if (!net_ix.emplace(ov->s, nets++).second) return false;  // two drivers
+        if (!net_ix.insert(*ov, nets++)) return false;  // two drivers
         R.pin_off.push_back((int64_t)R.pin_net.size());
-        R.gates.push_back(gn->s);
-        R.gate_cell.push_back(ci->second);
-        R.out_names.push_back(ov->s);
+        R.gates.add(gn);
+        R.gate_cell.push_back(ci);
+        R.outs.add(*ov);
         if (gp.eat(',')) continue;
         if (gp.eat(']')) break;
         return false;
@@ -373,12 +525,14 @@ inline bool read(const char *text, size_t len, const std::vector<Cell> &cells, R
   }
   for (auto &x : R.pin_net)
     if (x < 0) {
-      auto it = net_ix.find(pending[-1 - x]);
-      if (it == net_ix.end()) return false;  // undriven input
-      x = it->second;
+      const int64_t nx = net_ix.find(pending[-1 - x]);
+      if (nx < 0) return false;  // undriven input
+      x = nx;
     }
-  for (const auto &po : R.pos)
-    if (net_ix.find(po) == net_ix.end()) return false;
+  for (size_t i = 0; i < R.pos.size(); ++i)
+    if (net_ix.find(std::string_view(R.pos.blob).substr(R.pos.off[i],
+                                                        R.pos.off[i + 1] - R.pos.off[i])) < 0)
+      return false;
   return true;
 }
 
