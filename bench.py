@@ -14,7 +14,7 @@ shares of per-window input activity.
 A step = one pass of the hot path over the rank's windows: per window chunk
 K1 stimulus segmentation + one K4 gate-eval launch per (level, fanin group)
 with the toggle/dwell reduction fused, per-net sums accumulated on the device,
-and (N > 1) one NCCL all-reduce of those sums.  ``value`` has the stimulus
+and (N > 1) one NCCL all-reduce of those sums (``gs_allreduce_stats``).  ``value`` has the stimulus
 already resident in HBM (generated there, bit-identical to synth.stimulus);
 ``e2e`` takes it from pinned host memory through the C ABI every step
 (gs_stim_create: H2D + device validation) and reads the sums back.
@@ -326,11 +326,13 @@ def main():
     eng = _native.Engine(dev, 0, stream.cuda_stream)
     acc = torch.zeros(3 * N + 3, dtype=torch.int64, device="cuda")
 
+    comm = distributed.nccl_comm(device=local) if world > 1 else None
+
     def step(s):
         acc.zero_()
         eng.run_stats_device(s, 0, Wr, cfg.pct, acc.data_ptr())
-        if world > 1:
-            dist.all_reduce(acc)
+        if world > 1:  # the library's NCCL all-reduce of the device sums
+            comm.allreduce_stats(acc.data_ptr(), acc.numel(), stream.cuda_stream)
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):

@@ -370,6 +370,22 @@ int gs_netlist_copy(const gs_netlist *h, char *name, char *pis, int64_t *pis_off
                     int64_t *outs_off, int64_t *gate_cell, int64_t *pin_off, int64_t *pin_net);
 int gs_netlist_destroy(gs_netlist *h);
 
+/* ---- multi-GPU: the merge of the per-net sums across window shards ----- */
+
+/* The cross-GPU reduction of gs_run_stats_device accumulators (
+ * ActivityStats.merge, pkg/src/glsim/report.py:46-54): an in-place NCCL
+ * all-reduce (int64 sum) of acc_dev [n] on `stream` over `comm`, NVLink /
+ * NVSwitch between the GPUs of a box.  Integer addition is associative, so
+ * the merged sums -- and the SAIF -- are identical for any number of ranks.
+ * libnccl.so.2 is bound at run time; the communicator comes from
+ * gs_nccl_comm_create with an id made by gs_nccl_unique_id on one rank and
+ * broadcast to the others (e.g. over torch.distributed). */
+#define GS_NCCL_ID_BYTES 128
+int gs_nccl_unique_id(uint8_t *id);
+int gs_nccl_comm_create(const uint8_t *id, int nranks, int rank, int device, void **comm);
+int gs_nccl_comm_destroy(void *comm);
+int gs_allreduce_stats(int64_t *acc_dev, int64_t n, void *comm, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

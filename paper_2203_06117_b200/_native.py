@@ -145,6 +145,11 @@ SIGNATURES = {
     "gs_netlist_copy": (C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p, _i64p, C.c_char_p, _i64p,
                                   C.c_char_p, _i64p, C.c_char_p, _i64p, _i64p, _i64p, _i64p]),
     "gs_netlist_destroy": (C.c_int, [C.c_void_p]),
+    "gs_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "gs_nccl_comm_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int,
+                                      C.POINTER(C.c_void_p)]),
+    "gs_nccl_comm_destroy": (C.c_int, [C.c_void_p]),
+    "gs_allreduce_stats": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "gs_saif_format": (C.c_int, [C.c_char_p, _i64p, C.c_int64, _i64p, _i64p, _i64p, _i64p,
                                  C.c_int64, C.c_char_p, C.c_char_p, C.c_int, C.c_char_p,
                                  C.c_int64, _i64p]),
@@ -697,6 +702,35 @@ class Engine:
         t = Timing()
         _check(load().gs_last_timing(self.handle, C.byref(t)))
         return {f: getattr(t, f) for f, _ in Timing._fields_}
+
+
+NCCL_ID_BYTES = 128
+
+
+def nccl_unique_id():
+    """A new NCCL unique id (``gs_nccl_unique_id``), as bytes."""
+    buf = C.create_string_buffer(NCCL_ID_BYTES)
+    _check(load().gs_nccl_unique_id(buf))
+    return buf.raw
+
+
+class NcclComm:
+    """NCCL communicator of this rank (``gs_nccl_comm_create``); ``uid`` from
+    :func:`nccl_unique_id` on one rank, shared with all."""
+
+    def __init__(self, uid, nranks, rank, device=None):
+        lib = load()
+        h = C.c_void_p()
+        dev = current_device() if device is None else int(device)
+        _check(lib.gs_nccl_comm_create(bytes(uid), int(nranks), int(rank), dev, C.byref(h)))
+        self.handle = h
+        self._fin = weakref.finalize(self, lib.gs_nccl_comm_destroy, h)
+
+    def allreduce_stats(self, acc_ptr, n, stream=None):
+        """In-place int64 sum of the device accumulator at ``acc_ptr`` [n]
+        across the ranks (``gs_allreduce_stats``), on ``stream``."""
+        _check(load().gs_allreduce_stats(C.c_void_p(acc_ptr), int(n), self.handle,
+                                         C.c_void_p(stream) if stream else None))
 
 
 def dwell_sweep(arena, stimuli, boundaries, num_pis, num_gates):

@@ -5,6 +5,8 @@
 // then one K4 launch per logic level (the level barrier), all on one stream,
 // and synchronizes once at the chunk end to check the device-side flags.
 #include <algorithm>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <charconv>
 #include <cstdio>
 #include <cstdlib>
@@ -640,7 +642,10 @@ int64_t meta_bytes_per_window(const gs_design *d, bool arena) {
 // profiles/ab_tail.sh, round 1: C2 -3.0 %, C3 -0.7 %).
 constexpr int kItemCap = 12;   // tiles per item (profiles/ab_items_r01.log)
 constexpr int kItemDiv = 4;
-constexpr int kLeanItemCap = 8;  // super-tiles (of 4 tiles) per item of the lean kernels
+#ifndef GS_LEAN_ITEM_CAP
+#define GS_LEAN_ITEM_CAP 8  // (dev A/B knob)
+#endif
+constexpr int kLeanItemCap = GS_LEAN_ITEM_CAP;  // super-tiles (of 4 tiles) per item of the lean kernels
 
 struct ItemPlan {
   int tpi, ntg, tpi2, ntg2;
@@ -1916,6 +1921,100 @@ int gs_netlist_copy(const gs_netlist *h, char *name, char *pis, int64_t *pis_off
 
 int gs_netlist_destroy(gs_netlist *h) {
   delete h;
+  return GS_OK;
+}
+
+}  // extern "C"
+
+// =========================================================================
+// NCCL: the cross-GPU merge of the per-net sums (
+// ActivityStats.merge, report.py:46-54).  libnccl.so.2 is bound at run time
+// (dlopen), so the process's NCCL -- the one torch.distributed loaded, when
+// it did -- is the one used, and the library has no link-time NCCL dependency.
+
+namespace {
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId *);
+  ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int);
+  ncclResult_t (*commDestroy)(ncclComm_t);
+  ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
+                            ncclComm_t, cudaStream_t);
+  const char *(*getErrorString)(ncclResult_t);
+};
+
+int nccl_api(NcclApi **out) {
+  static NcclApi api;
+  static int state = 0;  // 0 unloaded, 1 ok, -1 unavailable
+  if (state == 0) {
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    state = -1;
+    if (h) {
+      api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+      api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+      api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+      api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+      if (api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce &&
+          api.getErrorString)
+        state = 1;
+    }
+  }
+  if (state != 1) return fail(GS_ERR_CUDA, "libnccl.so.2 is not available");
+  *out = &api;
+  return GS_OK;
+}
+
+int nccl_fail(NcclApi *api, ncclResult_t r, const char *what) {
+  return fail(GS_ERR_CUDA, std::string(what) + ": " + api->getErrorString(r));
+}
+}  // namespace
+
+extern "C" {
+
+int gs_nccl_unique_id(uint8_t *id) {
+  if (!id) return fail(GS_ERR_ARG, "null id buffer");
+  NcclApi *api;
+  TRY(nccl_api(&api));
+  ncclUniqueId u;
+  ncclResult_t r = api->getUniqueId(&u);
+  if (r != ncclSuccess) return nccl_fail(api, r, "ncclGetUniqueId");
+  static_assert(sizeof(u.internal) == GS_NCCL_ID_BYTES, "NCCL unique id size");
+  memcpy(id, u.internal, GS_NCCL_ID_BYTES);
+  return GS_OK;
+}
+
+int gs_nccl_comm_create(const uint8_t *id, int nranks, int rank, int device, void **comm) {
+  if (!id || !comm || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(GS_ERR_ARG, "bad NCCL communicator arguments");
+  *comm = nullptr;
+  NcclApi *api;
+  TRY(nccl_api(&api));
+  TRY(use_device(device));
+  ncclUniqueId u;
+  memcpy(u.internal, id, GS_NCCL_ID_BYTES);
+  ncclComm_t c = nullptr;
+  ncclResult_t r = api->commInitRank(&c, nranks, u, rank);
+  if (r != ncclSuccess) return nccl_fail(api, r, "ncclCommInitRank");
+  *comm = (void *)c;
+  return GS_OK;
+}
+
+int gs_nccl_comm_destroy(void *comm) {
+  if (!comm) return GS_OK;
+  NcclApi *api;
+  TRY(nccl_api(&api));
+  api->commDestroy((ncclComm_t)comm);
+  return GS_OK;
+}
+
+int gs_allreduce_stats(int64_t *acc_dev, int64_t n, void *comm, void *stream) {
+  if (!acc_dev || n < 0 || !comm) return fail(GS_ERR_ARG, "bad all-reduce arguments");
+  NcclApi *api;
+  TRY(nccl_api(&api));
+  ncclResult_t r = api->allReduce(acc_dev, acc_dev, (size_t)n, ncclInt64, ncclSum,
+                                  (ncclComm_t)comm, (cudaStream_t)stream);
+  if (r != ncclSuccess) return nccl_fail(api, r, "ncclAllReduce");
   return GS_OK;
 }
 

@@ -35,8 +35,11 @@
 namespace gs {
 
 // CTAs of 4 warps per SM each fixed-K instance is built for (launch bounds)
+#ifndef GS_LEAN_CTAS2
+#define GS_LEAN_CTAS2 8   // CTAs per SM of the k <= 2 instances (dev A/B knob)
+#endif
 template <int K>
-__host__ __device__ constexpr int lean_ctas() { return K <= 2 ? 8 : K == 3 ? 7 : 6; }
+__host__ __device__ constexpr int lean_ctas() { return K <= 2 ? GS_LEAN_CTAS2 : K == 3 ? 7 : 6; }
 
 constexpr int kSuper = kEvalWarps;         // tiles per CTA step (one per warp)
 constexpr int kPool = kSuper * kTile;      // windows per CTA step
@@ -666,6 +669,21 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         const unsigned L = (nl + kWarp - 1) & ~(unsigned)(kWarp - 1);
         GS_PROF_ADD(PF_LOOP_WINDOWS, warp == 0 ? nl : 0);
         GS_PROF_ADD(PF_TRIVIAL, warp == 0 ? n2 : 0);
+#ifdef GS_LEAN_MSPREAD
+        // loop windows dealt round-robin over the warps (lane-major), so the
+        // long event loops are spread instead of packed into one warp
+        (void)L;
+        for (unsigned i = lane * kEvalWarps + warp; i < nl; i += kEvalThreads) {
+          const unsigned e = S.s.list[0][i];
+          loop_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
+                                             (int)(e & 127u), (e >> 7) & 15u, acc);
+        }
+        for (unsigned i = tid; i < n2; i += kEvalThreads) {
+          const unsigned e = S.s.list[1][i];
+          two_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
+                                            (int)(e & 127u), (e >> 7) & 15u, acc);
+        }
+#else
         for (unsigned i = tid; i < L + n2; i += kEvalThreads) {
           if (i < nl) {
             const unsigned e = S.s.list[0][i];
@@ -677,6 +695,7 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
                                               (int)(e & 127u), (e >> 7) & 15u, acc);
           }
         }
+#endif
       }
       GS_PROF_T(pt2);
       GS_PROF_ADD(PF_LOOP, pt2 - pt1);

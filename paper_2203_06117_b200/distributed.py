@@ -65,16 +65,31 @@ def allreduce_sum(vec, group=None, device=None):
     return t.cpu().numpy()
 
 
+def nccl_comm(group=None, device=None):
+    """This rank's NCCL communicator over the process group (ids shared over
+    torch.distributed): the one :func:`simulate_sharded` all-reduces the
+    device sums with (``gs_allreduce_stats``)."""
+    import torch.distributed as dist
+    from . import _native
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    box = [_native.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0,
+                               group=group)
+    return _native.NcclComm(box[0], world, rank, device)
+
+
 def simulate_sharded(model, stimuli, pct=100, group=None, runner=None, device=None,
-                     balance=True):
+                     balance=True, comm=None):
     """Per-net statistics of all windows, computed as this rank's shard plus one
     all-reduce.
 
     Default (``runner`` None): the GPU engine of this process's device adds
     the shard's sums into a device int64 buffer ``[t1 | tc | ig | 3 totals]``
-    (``gs_run_stats_device``), the buffer is all-reduced where it lies (NCCL
-    over NVLink with the ``nccl`` backend), and one device-to-host copy
-    returns the merged result.  A ``runner(w_lo, w_hi) -> (t1, tc, ig,
+    (``gs_run_stats_device``), the buffer is all-reduced where it lies -- by
+    the library's NCCL all-reduce (``gs_allreduce_stats``) over ``comm`` when
+    given (:func:`nccl_comm`), else by the process group's all-reduce -- and
+    one device-to-host copy returns the merged result.  A ``runner(w_lo, w_hi) -> (t1, tc, ig,
     totals)`` (host arrays) replaces the engine, e.g. the CPU oracle in the
     gloo tests.  Returns ``((t1, tc, ig, totals), (lo, hi))``.
     """
@@ -94,7 +109,12 @@ def simulate_sharded(model, stimuli, pct=100, group=None, runner=None, device=No
             # synchronous on the engine's stream: acc is complete on return
             s.engine.run_stats_device(s.stim, lo, hi, int(pct), acc.data_ptr())
         if world > 1:
-            dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+            if comm is not None:  # the library's own NCCL all-reduce
+                torch.cuda.synchronize(dev)
+                comm.allreduce_stats(acc.data_ptr(), acc.numel(),
+                                     torch.cuda.current_stream(dev).cuda_stream)
+            else:
+                dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
         return unpack(acc.cpu().numpy(), N), (lo, hi)
     if hi > lo:
         vec = pack(*runner(lo, hi))

@@ -140,3 +140,29 @@ def test_two_rank_gpu_runner_equals_single_run():
             for a, x in zip(arrs, ref[:3]):
                 assert np.array_equal(a, x)
             assert tuple(totals) == tuple(ref[3])
+
+
+@pytest.mark.gpu
+def test_library_nccl_allreduce_single_rank():
+    # gs_nccl_unique_id / gs_nccl_comm_create / gs_allreduce_stats on a
+    # one-rank communicator: the in-place int64 sum is the identity, and the
+    # sharded runner takes the library's all-reduce path with it
+    import torch
+    import gen
+    import paper_2203_06117_b200 as api
+    from paper_2203_06117_b200 import _native
+    uid = _native.nccl_unique_id()
+    assert len(uid) == _native.NCCL_ID_BYTES
+    comm = _native.NcclComm(uid, 1, 0)
+    x = torch.arange(-5, 1000, dtype=torch.int64, device="cuda") * 7919
+    y = x.clone()
+    comm.allreduce_stats(y.data_ptr(), y.numel(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(x, y)
+    docs = gen.make_docs(4242, n_gates=400, n_pis=8, windows=40, duration_ps=20_000,
+                         max_toggles=300)
+    nl, lv, delays, waves, duration, b, stim = gen.load(docs, api)
+    model = api.compile_design(lv, delays)
+    (t1, tc, ig, tot), _ = distributed.simulate_sharded(model, stim, docs.pct, comm=comm)
+    ref = api.simulate_stats(model, stim, pathpulse_pct=docs.pct)
+    assert np.array_equal(t1, ref[0]) and np.array_equal(tc, ref[1]) and tot == ref[3]
