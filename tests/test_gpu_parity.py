@@ -379,3 +379,27 @@ def test_store_pass_with_foreign_capacities_simulates_and_checks():
     arena = api.allocate_arena(caps, model.order, stim.boundaries, (0, stim.num_windows), lv)
     with pytest.raises(api.ConsistencyError):
         simcore.store_pass(model, stim, None, arena)
+
+
+def test_stats_then_arena_on_one_engine_resizes_the_chunk():
+    # a stats run sizes its window chunk for stats metadata; an arena run on
+    # the same engine must size its own (arena metadata is ~50 B per
+    # gate-window more) instead of reusing the stats chunk and running out of
+    # its budget
+    from paper_2203_06117_b200 import _native, synth
+    cfg = synth.config("C2", gates=20_000, levels=8, windows=4096)
+    m = synth.design(cfg)
+    dev = m.device()
+    budget = 256 << 20
+    eng = _native.Engine(dev, budget)
+    st = _native.SynthStimulus(dev, cfg, 0, 4096)
+    ref = eng.run_stats(st, 0, 4096, cfg.pct)
+    stats_chunks = eng.timing()["chunks"]
+    r = eng.run_arena(st, 0, 4096, cfg.pct, want_stats=True)
+    assert eng.timing()["chunks"] > stats_chunks
+    for a, b in zip(r["stats"][:3], ref[:3]):
+        assert np.array_equal(a, b)
+    again = eng.run_stats(st, 0, 4096, cfg.pct)
+    assert eng.timing()["chunks"] <= stats_chunks
+    for a, b in zip(again[:3], ref[:3]):
+        assert np.array_equal(a, b)
