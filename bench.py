@@ -505,6 +505,11 @@ def main():
                         e2e_upload_ms + e2e_run_ms,
                         "host_ms_stim_upload": e2e_upload_ms, "host_ms_run": e2e_run_ms},
                 "clocks": clocks, "gpu_launches": launches,
+                "cuda_graphs": {"chunk_graphs_built": timing["graph_builds"],
+                                "chunk_graph_replays": timing["graph_replays"],
+                                "note": "each window chunk's launch sequence (K1 + every "
+                                        "level's K4 launches) is one CUDA graph, built on "
+                                        "first use and replayed"},
                 "activity": {"input_toggles_per_gw": in_tog / (cfg.gates * Wr),
                              "output_toggles_per_gw": out_tog / (cfg.gates * Wr),
                              "chunks_per_step": timing["chunks"]}}

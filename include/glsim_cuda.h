@@ -119,6 +119,8 @@ typedef struct gs_timing {
   int64_t data_bytes_peak; /* high-water device waveform pool usage            */
   int64_t input_toggles; /* sum over gate-windows of fanin toggles (n_in)      */
   int64_t output_toggles;/* stored output toggles                              */
+  int64_t graph_builds;  /* chunk launch sequences captured as CUDA graphs     */
+  int64_t graph_replays; /* chunk graphs replayed from the engine's cache      */
 } gs_timing;
 
 /* ---- library ---------------------------------------------------------- */
@@ -249,6 +251,28 @@ int gs_dwell_sweep(int64_t num_nets, const uint8_t *net_kind, const int64_t *net
                    int64_t num_gates, int64_t g_cols,
                    const int64_t *boundaries, int64_t w_lo, int64_t w_hi, int64_t w_off,
                    int64_t *t0_out, int64_t *t1_out, int64_t *tc_out);
+
+/* sim_span (_kernels.py:17-210): Algo. 1 for gates order[oi_lo:oi_hi] over
+ * windows [w_lo, w_hi) on the reference's own layout and argument list --
+ * host arrays in and out, executed on the GPU (one thread per gate-window),
+ * for code that drives the reference's per-level loop (simcore.py:295-325)
+ * itself.  2-D arrays are row-major with the given column counts: stim_off /
+ * stim_cnt [stim_rows, stim_cols], init_vals [num_nets, init_cols], g_* and
+ * out_* [num_gates, g_cols] (column = window - w_off).  gbuf / g_cnt / out_*
+ * are read and written back whole; out_err is only set (to 1).  Every index
+ * the span follows is checked on the host first (GS_ERR_ARG). */
+int gs_sim_span(int64_t oi_lo, int64_t oi_hi, int64_t w_lo, int64_t w_hi, int64_t w_off,
+                const int64_t *order, int64_t num_gates, const int64_t *pin_off,
+                const int64_t *pin_net, const int64_t *pin_ic, const int64_t *pin_arc,
+                const int64_t *arc_rows, int64_t num_arc_rows, const int64_t *lut_off,
+                const uint8_t *lut_bits, int64_t num_lut_bits, const int64_t *out_net,
+                const uint8_t *net_kind, const int64_t *net_slot, int64_t num_nets,
+                const int64_t *stim_buf, int64_t n_stim_buf, const int64_t *stim_off,
+                const int64_t *stim_cnt, int64_t stim_rows, int64_t stim_cols,
+                const uint8_t *init_vals, int64_t init_cols, const int64_t *boundaries,
+                int64_t *gbuf, int64_t n_gbuf, const int64_t *g_off, const int64_t *g_cap,
+                int64_t *g_cnt, int64_t g_cols, int64_t *out_filt, int64_t *out_icf,
+                int64_t *out_disc, int64_t *out_err, int64_t *out_peak, int64_t pct);
 
 /* init_values (_kernels.py:213-231): zero-delay window-start value of every
  * net; vals_out is [num_nets, W] uint8, rows < P copied from stim_init [P, W]. */

@@ -82,7 +82,8 @@ class Timing(C.Structure):
     _fields_ = [("ms_total", C.c_float), ("ms_gate_eval", C.c_float), ("ms_stim", C.c_float),
                 ("launches", C.c_int64), ("gate_eval_launches", C.c_int64),
                 ("chunks", C.c_int64), ("data_bytes_peak", C.c_int64),
-                ("input_toggles", C.c_int64), ("output_toggles", C.c_int64)]
+                ("input_toggles", C.c_int64), ("output_toggles", C.c_int64),
+                ("graph_builds", C.c_int64), ("graph_replays", C.c_int64)]
 
 
 # every symbol include/glsim_cuda.h declares, with its ctypes signature
@@ -118,6 +119,13 @@ SIGNATURES = {
                                  C.c_int64, C.c_int64, _i64p, C.c_int64, C.c_int64, C.c_int64,
                                  _i64p, _i64p, _i64p]),
     "gs_init_values": (C.c_int, [C.POINTER(DesignDesc), _u8p, C.c_int64, _u8p]),
+    "gs_sim_span": (C.c_int, [C.c_int64] * 5 + [_i64p, C.c_int64, _i64p, _i64p, _i64p, _i64p,
+                                                _i64p, C.c_int64, _i64p, _u8p, C.c_int64,
+                                                _i64p, _u8p, _i64p, C.c_int64, _i64p,
+                                                C.c_int64, _i64p, _i64p, C.c_int64, C.c_int64,
+                                                _u8p, C.c_int64, _i64p, _i64p, C.c_int64,
+                                                _i64p, _i64p, _i64p, C.c_int64, _i64p, _i64p,
+                                                _i64p, _i64p, _i64p, C.c_int64]),
     "gs_vcd_parse": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(C.c_char_p), C.c_int64,
                                C.POINTER(C.c_void_p)]),
     "gs_vcd_sizes": (C.c_int, [C.c_void_p, _i64p, _i64p]),
@@ -757,6 +765,36 @@ def dwell_sweep(arena, stimuli, boundaries, num_pis, num_gates):
     if num_gates:
         ig[num_pis:] = np.asarray(arena.filtered, dtype=np.int64).sum(axis=1)
     return t1, tc, ig
+
+
+def sim_span(oi_lo, oi_hi, w_lo, w_hi, w_off, order, pin_off, pin_net, pin_ic, pin_arc,
+             arc_rows, lut_off, lut_bits, out_net, net_kind, net_slot, stim_buf, stim_off,
+             stim_cnt, init_vals, boundaries, gbuf, g_off, g_cap, g_cnt, out_filt, out_icf,
+             out_disc, out_err, out_peak, pct):
+    """The reference kernel ``sim_span`` (``_kernels.py:17-210``) with its own
+    argument list, on the GPU (``gs_sim_span``): arrays as the reference
+    passes them (numpy, int64 / uint8, 2-D row-major); outputs written in
+    place."""
+    c = [_c64(a) for a in (order, pin_off, pin_net, pin_ic, pin_arc, arc_rows, lut_off, out_net,
+                           net_slot, stim_buf, stim_off, stim_cnt, boundaries, g_off, g_cap)]
+    order, pin_off, pin_net, pin_ic, pin_arc, arc_rows, lut_off, out_net, net_slot, \
+        stim_buf, stim_off, stim_cnt, boundaries, g_off, g_cap = c
+    u = [_c8(a) for a in (lut_bits, net_kind, init_vals)]
+    lut_bits, net_kind, init_vals = u
+    outs = (gbuf, g_cnt, out_filt, out_icf, out_disc, out_err, out_peak)
+    for a in outs:
+        if a.dtype != np.int64 or not a.flags.c_contiguous:
+            raise ValueError("sim_span outputs must be C-contiguous int64 arrays")
+    G = order.size
+    _check(load().gs_sim_span(
+        int(oi_lo), int(oi_hi), int(w_lo), int(w_hi), int(w_off), _p64(order), G,
+        _p64(pin_off), _p64(pin_net), _p64(pin_ic), _p64(pin_arc), _p64(arc_rows),
+        arc_rows.size // 2, _p64(lut_off), _p8(lut_bits), lut_bits.size, _p64(out_net),
+        _p8(net_kind), _p64(net_slot), net_kind.size, _p64(stim_buf), stim_buf.size,
+        _p64(stim_off), _p64(stim_cnt), stim_off.shape[0], stim_off.shape[1],
+        _p8(init_vals), init_vals.shape[1], _p64(boundaries), _p64(gbuf), gbuf.size,
+        _p64(g_off), _p64(g_cap), _p64(g_cnt), g_off.shape[1], _p64(out_filt), _p64(out_icf),
+        _p64(out_disc), _p64(out_err), _p64(out_peak), int(pct)))
 
 
 def init_values(model, stim_init):

@@ -8,6 +8,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 #include <charconv>
+#include <map>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -459,6 +460,20 @@ struct gs_engine {
     std::vector<int64_t> piece;   // gate-major (arena order), absolute times
   };
   std::vector<ArenaPiece> kept;
+  // one CUDA graph per distinct chunk launch sequence (K1 + every level's K4
+  // launches + the chunk's resets and events), keyed by the exact launch
+  // parameters; a replay skips the per-launch host cost and the gaps
+  struct ChunkGraph {
+    cudaGraphExec_t exec = nullptr;
+    int k1 = 0, nl = 0;
+  };
+  std::map<std::string, ChunkGraph> graphs;
+  int64_t graph_hits = 0, graph_builds = 0;
+  void drop_graphs() {
+    for (auto &kv : graphs)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    graphs.clear();
+  }
   const gs_stim *kept_stim = nullptr;
   int64_t kept_lo = 0, kept_hi = 0;
   int kept_pct = -1;
@@ -495,6 +510,7 @@ struct gs_engine {
     bump_host = nullptr;
     for (auto &e : ev)
       if (e) cudaEventDestroy(e), e = nullptr;
+    drop_graphs();
     if (own_stream && st) cudaStreamDestroy(st);
     st = nullptr;
   }
@@ -850,75 +866,114 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
                                ro.arena_cols * 8, wc * 8, G, cudaMemcpyHostToDevice, e->st));
       }
     }
-    CK(cudaMemsetAsync(e->acc, 0, sizeof(long long) * ACC_ROWS * N, e->st));
-    CK(cudaMemsetAsync(e->bump, 0, sizeof(unsigned long long) * (2 * (size_t)nregions + 1), e->st));
-    CK(cudaMemsetAsync(e->work, 0, sizeof(unsigned) * (D->L * 5 + 1), e->st));
-    CK(cudaMemsetAsync(e->err, 0, sizeof(int) * ERR_NFLAGS, e->st));
-    CK(cudaEventRecord(e->ev[0], e->st));
-    if (narrow) {
-      chunk_windows<<<(int)((Wpad + 255) / 256), 256, 0, e->st>>>(C);
-      CK(cudaGetLastError());
-    }
-    // ---- K1
-    int k1 = 0;
-    if (s->P > 0) {
-      const int tpi = std::max(1, std::min(Tc, 4));
-      const int ntg = (Tc + tpi - 1) / tpi;
-      const int64_t items = (int64_t)s->P * ntg;
-      if (s->csr) {
-        const int blocks = (int)std::min<int64_t>((items + 7) / 8, (int64_t)e->sms * 16);
-        stim_segment_csr<TS><<<blocks, 256, 0, e->st>>>(Sd, C, tpi, ntg);
-      } else {
-        stim_segment_win<TS><<<ncta, kEvalThreads, 0, e->st>>>(Sd, C, tpi, ntg);
+    int k1 = 0, nl = 0;
+    auto enqueue = [&]() -> int {
+      CK(cudaMemsetAsync(e->acc, 0, sizeof(long long) * ACC_ROWS * N, e->st));
+      CK(cudaMemsetAsync(e->bump, 0, sizeof(unsigned long long) * (2 * (size_t)nregions + 1), e->st));
+      CK(cudaMemsetAsync(e->work, 0, sizeof(unsigned) * (D->L * 5 + 1), e->st));
+      CK(cudaMemsetAsync(e->err, 0, sizeof(int) * ERR_NFLAGS, e->st));
+      CK(cudaEventRecordWithFlags(e->ev[0], e->st, cudaEventRecordExternal));
+      if (narrow) {
+        chunk_windows<<<(int)((Wpad + 255) / 256), 256, 0, e->st>>>(C);
+        CK(cudaGetLastError());
       }
-      CK(cudaGetLastError());
-      k1 = 1;
-    }
-    CK(cudaEventRecord(e->ev[1], e->st));
-    // ---- K4: per level, one launch per fanin-count group (the launch
-    // boundary between levels is the level barrier)
-    int nl = 0;
-    const int STc = (Tc + kSuper - 1) / kSuper;
-    for (int l = 0; l < D->L; ++l) {
-      for (int gi = 0; gi < 5; ++gi) {
-        const int lo = (int)D->grp[l * 6 + gi];
-        const int n = (int)(D->grp[l * 6 + gi + 1] - lo);
-        if (n <= 0) continue;
-        const bool lean = narrow && gi < 4;
-        LevelArgs A;
-        A.lo = lo;
-        A.n = n;
-        // work items: (gate, run of tiles) for the generic kernel, (gate, run
-        // of 4-tile super-tiles) for the lean kernels, whose CTA is the worker
-        const ItemPlan ip = plan_items(n, lean ? STc : Tc,
-                                       e->item_workers > 0 ? e->item_workers
-                                                           : (lean ? ncta : nregions),
-                                       lean ? kLeanItemCap : kItemCap, e->tail_div,
-                                       e->tail_frac);
-        A.tpi = ip.tpi;
-        A.ntg = ip.ntg;
-        A.tpi2 = ip.tpi2;
-        A.ntg2 = ip.ntg2;
-        A.pct = pct;
-        A.counter = l * 5 + gi;
-        const int sm = e->sms;
-        if (narrow && p100 && gi < 4) {
-          if (gi == 0) TRY((launch_lean<MODE, 1, true>(sm, e->st, Dd, C, A, ncta)));
-          if (gi == 1) TRY((launch_lean<MODE, 2, true>(sm, e->st, Dd, C, A, ncta)));
-          if (gi == 2) TRY((launch_lean<MODE, 3, true>(sm, e->st, Dd, C, A, ncta)));
-          if (gi == 3) TRY((launch_lean<MODE, 4, true>(sm, e->st, Dd, C, A, ncta)));
-        } else if (narrow && gi < 4) {
-          if (gi == 0) TRY((launch_lean<MODE, 1, false>(sm, e->st, Dd, C, A, ncta)));
-          if (gi == 1) TRY((launch_lean<MODE, 2, false>(sm, e->st, Dd, C, A, ncta)));
-          if (gi == 2) TRY((launch_lean<MODE, 3, false>(sm, e->st, Dd, C, A, ncta)));
-          if (gi == 3) TRY((launch_lean<MODE, 4, false>(sm, e->st, Dd, C, A, ncta)));
+      // ---- K1
+      if (s->P > 0) {
+        const int tpi = std::max(1, std::min(Tc, 4));
+        const int ntg = (Tc + tpi - 1) / tpi;
+        const int64_t items = (int64_t)s->P * ntg;
+        if (s->csr) {
+          const int blocks = (int)std::min<int64_t>((items + 7) / 8, (int64_t)e->sms * 16);
+          stim_segment_csr<TS><<<blocks, 256, 0, e->st>>>(Sd, C, tpi, ntg);
         } else {
-          TRY((launch_eval<TS, long long, MODE, 0, false>(sm, e->st, Dd, C, A, ncta)));
+          stim_segment_win<TS><<<ncta, kEvalThreads, 0, e->st>>>(Sd, C, tpi, ntg);
         }
-        ++nl;
+        CK(cudaGetLastError());
+        k1 = 1;
       }
+      CK(cudaEventRecordWithFlags(e->ev[1], e->st, cudaEventRecordExternal));
+      // ---- K4: per level, one launch per fanin-count group (the launch
+      // boundary between levels is the level barrier)
+      const int STc = (Tc + kSuper - 1) / kSuper;
+      for (int l = 0; l < D->L; ++l) {
+        for (int gi = 0; gi < 5; ++gi) {
+          const int lo = (int)D->grp[l * 6 + gi];
+          const int n = (int)(D->grp[l * 6 + gi + 1] - lo);
+          if (n <= 0) continue;
+          const bool lean = narrow && gi < 4;
+          LevelArgs A;
+          A.lo = lo;
+          A.n = n;
+          // work items: (gate, run of tiles) for the generic kernel, (gate, run
+          // of 4-tile super-tiles) for the lean kernels, whose CTA is the worker
+          const ItemPlan ip = plan_items(n, lean ? STc : Tc,
+                                         e->item_workers > 0 ? e->item_workers
+                                                             : (lean ? ncta : nregions),
+                                         lean ? kLeanItemCap : kItemCap, e->tail_div,
+                                         e->tail_frac);
+          A.tpi = ip.tpi;
+          A.ntg = ip.ntg;
+          A.tpi2 = ip.tpi2;
+          A.ntg2 = ip.ntg2;
+          A.pct = pct;
+          A.counter = l * 5 + gi;
+          const int sm = e->sms;
+          if (narrow && p100 && gi < 4) {
+            if (gi == 0) TRY((launch_lean<MODE, 1, true>(sm, e->st, Dd, C, A, ncta)));
+            if (gi == 1) TRY((launch_lean<MODE, 2, true>(sm, e->st, Dd, C, A, ncta)));
+            if (gi == 2) TRY((launch_lean<MODE, 3, true>(sm, e->st, Dd, C, A, ncta)));
+            if (gi == 3) TRY((launch_lean<MODE, 4, true>(sm, e->st, Dd, C, A, ncta)));
+          } else if (narrow && gi < 4) {
+            if (gi == 0) TRY((launch_lean<MODE, 1, false>(sm, e->st, Dd, C, A, ncta)));
+            if (gi == 1) TRY((launch_lean<MODE, 2, false>(sm, e->st, Dd, C, A, ncta)));
+            if (gi == 2) TRY((launch_lean<MODE, 3, false>(sm, e->st, Dd, C, A, ncta)));
+            if (gi == 3) TRY((launch_lean<MODE, 4, false>(sm, e->st, Dd, C, A, ncta)));
+          } else {
+            TRY((launch_eval<TS, long long, MODE, 0, false>(sm, e->st, Dd, C, A, ncta)));
+          }
+          ++nl;
+        }
+      }
+      CK(cudaEventRecordWithFlags(e->ev[2], e->st, cudaEventRecordExternal));
+      return GS_OK;
+    };
+    {
+      // the chunk's launch sequence as a CUDA graph, cached by its exact
+      // parameters (pointers, sizes, item plans follow from them)
+      std::string key((const char *)&C, sizeof(C));
+      const int64_t extra[] = {(int64_t)(intptr_t)D, (int64_t)(intptr_t)s->bnd,
+                               (int64_t)(intptr_t)s->pi_off, (int64_t)(intptr_t)s->pi_times,
+                               (int64_t)(intptr_t)s->buf, (int64_t)(intptr_t)s->offsets,
+                               s->P, s->W, s->csr, pct, MODE, (int64_t)sizeof(TS), narrow,
+                               ncta, nregions, e->item_workers, e->tail_div, e->tail_frac};
+      key.append((const char *)extra, sizeof(extra));
+      auto it = e->graphs.find(key);
+      if (it == e->graphs.end()) {
+        if (e->graphs.size() >= 64) e->drop_graphs();
+        cudaGraph_t gr = nullptr;
+        CK(cudaStreamBeginCapture(e->st, cudaStreamCaptureModeThreadLocal));
+        const int rc = enqueue();
+        const cudaError_t ce = cudaStreamEndCapture(e->st, &gr);
+        if (rc != GS_OK) {
+          if (gr) cudaGraphDestroy(gr);
+          return rc;
+        }
+        CK(ce);
+        gs_engine::ChunkGraph cg;
+        const cudaError_t ie = cudaGraphInstantiate(&cg.exec, gr, 0);
+        cudaGraphDestroy(gr);
+        CK(ie);
+        cg.k1 = k1;
+        cg.nl = nl;
+        it = e->graphs.emplace(std::move(key), cg).first;
+        ++e->graph_builds;
+      } else {
+        ++e->graph_hits;
+      }
+      k1 = it->second.k1;
+      nl = it->second.nl;
+      CK(cudaGraphLaunch(it->second.exec, e->st));
     }
-    CK(cudaEventRecord(e->ev[2], e->st));
     CK(cudaMemcpyAsync(e->err_host, e->err, sizeof(int) * ERR_NFLAGS, cudaMemcpyDeviceToHost, e->st));
     unsigned long long blocks_used = 0;
     CK(cudaMemcpyAsync(&blocks_used, e->bump + 2 * (size_t)nregions, sizeof(unsigned long long),
@@ -1001,6 +1056,8 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
   e->last.gate_eval_launches = eval_launches;
   e->last.chunks = chunks;
   e->last.data_bytes_peak = peak_bytes;
+  e->last.graph_builds = e->graph_builds;
+  e->last.graph_replays = e->graph_hits;
   return GS_OK;
 }
 
@@ -1526,6 +1583,114 @@ int gs_dwell_sweep(int64_t num_nets, const uint8_t *net_kind, const int64_t *net
   }();
   dfree(nk); dfree(ns); dfree(sb); dfree(so); dfree(sc); dfree(si); dfree(gb); dfree(go);
   dfree(gc); dfree(gi); dfree(bd); dfree(out);
+  return rc;
+}
+
+int gs_sim_span(int64_t oi_lo, int64_t oi_hi, int64_t w_lo, int64_t w_hi, int64_t w_off,
+                const int64_t *order, int64_t num_gates, const int64_t *pin_off,
+                const int64_t *pin_net, const int64_t *pin_ic, const int64_t *pin_arc,
+                const int64_t *arc_rows, int64_t num_arc_rows, const int64_t *lut_off,
+                const uint8_t *lut_bits, int64_t num_lut_bits, const int64_t *out_net,
+                const uint8_t *net_kind, const int64_t *net_slot, int64_t num_nets,
+                const int64_t *stim_buf, int64_t n_stim_buf, const int64_t *stim_off,
+                const int64_t *stim_cnt, int64_t stim_rows, int64_t stim_cols,
+                const uint8_t *init_vals, int64_t init_cols, const int64_t *boundaries,
+                int64_t *gbuf, int64_t n_gbuf, const int64_t *g_off, const int64_t *g_cap,
+                int64_t *g_cnt, int64_t g_cols, int64_t *out_filt, int64_t *out_icf,
+                int64_t *out_disc, int64_t *out_err, int64_t *out_peak, int64_t pct) {
+  (void)out_net;  // gate g drives net out_net[g]; sim_span itself never reads it
+  const int64_t G = num_gates, N = num_nets;
+  if (oi_lo < 0 || oi_hi > G || oi_lo > oi_hi || w_lo < 0 || w_hi < w_lo ||
+      w_hi > stim_cols || w_hi > init_cols || w_off > w_lo || w_hi - w_off > g_cols ||
+      pct < 0 || pct > 100 || G < 0 || N < G || n_gbuf < 0 || n_stim_buf < 0)
+    return fail(GS_ERR_ARG, "sim_span range or size out of bounds");
+  // every index the span will follow, checked before anything reaches the GPU
+  const int64_t n_pins = G ? pin_off[G] : 0;
+  for (int64_t oi = oi_lo; oi < oi_hi; ++oi) {
+    const int64_t g = order[oi];
+    if (g < 0 || g >= G) return fail(GS_ERR_ARG, "order entry out of range");
+    const int64_t p0 = pin_off[g], k = pin_off[g + 1] - p0;
+    if (k < 1 || k > kMaxK || p0 < 0 || p0 + k > n_pins)
+      return fail(GS_ERR_ARG, "gate fanin count out of range");
+    if (lut_off[g] < 0 || lut_off[g] + (int64_t(1) << k) > num_lut_bits)
+      return fail(GS_ERR_ARG, "lut_off out of range");
+    for (int64_t p = p0; p < p0 + k; ++p) {
+      const int64_t n = pin_net[p];
+      if (n < 0 || n >= N || pin_arc[p] < 0 ||
+          pin_arc[p] + (int64_t(1) << (k - 1)) > num_arc_rows)
+        return fail(GS_ERR_ARG, "pin entry out of range");
+      const int64_t sl = net_slot[n];
+      for (int64_t w = w_lo; w < w_hi; ++w) {
+        int64_t o, c, lim;
+        if (net_kind[n] == 0) {
+          if (sl < 0 || sl >= stim_rows) return fail(GS_ERR_ARG, "input slot out of range");
+          o = stim_off[sl * stim_cols + w], c = stim_cnt[sl * stim_cols + w], lim = n_stim_buf;
+        } else {
+          if (sl < 0 || sl >= G) return fail(GS_ERR_ARG, "gate slot out of range");
+          o = g_off[sl * g_cols + (w - w_off)], c = g_cnt[sl * g_cols + (w - w_off)];
+          lim = n_gbuf;
+        }
+        if (o < 0 || c < 0 || o + c > lim) return fail(GS_ERR_ARG, "fanin region out of range");
+      }
+    }
+    for (int64_t w = w_lo; w < w_hi; ++w) {
+      const int64_t o = g_off[g * g_cols + (w - w_off)], c = g_cap[g * g_cols + (w - w_off)];
+      if (o < 0 || c < 0 || o + c > n_gbuf) return fail(GS_ERR_ARG, "output region out of range");
+    }
+  }
+  TRY(use_device(0));
+  std::vector<void *> bufs;
+  auto up = [&](const void *src, size_t bytes, void **dst) -> int {
+    *dst = nullptr;
+    CK(cudaMalloc(dst, bytes ? bytes : 8));
+    bufs.push_back(*dst);
+    if (bytes && src) CK(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+    return GS_OK;
+  };
+  const size_t gw = (size_t)(G * g_cols) * 8, nw = (size_t)N;
+  int rc = [&]() -> int {
+    SpanArgs A;
+    void *p;
+    A.oi_lo = oi_lo; A.oi_hi = oi_hi; A.w_lo = w_lo; A.w_hi = w_hi; A.w_off = w_off;
+    A.stim_cols = stim_cols; A.init_cols = init_cols; A.g_cols = g_cols; A.pct = pct;
+    TRY(up(order, (size_t)G * 8, &p)); A.order = (const long long *)p;
+    TRY(up(pin_off, (size_t)(G + 1) * 8, &p)); A.pin_off = (const long long *)p;
+    TRY(up(pin_net, (size_t)n_pins * 8, &p)); A.pin_net = (const long long *)p;
+    TRY(up(pin_ic, (size_t)n_pins * 8, &p)); A.pin_ic = (const long long *)p;
+    TRY(up(pin_arc, (size_t)n_pins * 8, &p)); A.pin_arc = (const long long *)p;
+    TRY(up(arc_rows, (size_t)num_arc_rows * 16, &p)); A.arc_rows = (const long long *)p;
+    TRY(up(lut_off, (size_t)G * 8, &p)); A.lut_off = (const long long *)p;
+    TRY(up(lut_bits, (size_t)num_lut_bits, &p)); A.lut_bits = (const unsigned char *)p;
+    TRY(up(net_kind, nw, &p)); A.net_kind = (const unsigned char *)p;
+    TRY(up(net_slot, nw * 8, &p)); A.net_slot = (const long long *)p;
+    TRY(up(stim_buf, (size_t)n_stim_buf * 8, &p)); A.stim_buf = (const long long *)p;
+    TRY(up(stim_off, (size_t)(stim_rows * stim_cols) * 8, &p)); A.stim_off = (const long long *)p;
+    TRY(up(stim_cnt, (size_t)(stim_rows * stim_cols) * 8, &p)); A.stim_cnt = (const long long *)p;
+    TRY(up(init_vals, nw * (size_t)init_cols, &p)); A.init_vals = (const unsigned char *)p;
+    TRY(up(boundaries, (size_t)(stim_cols + 1) * 8, &p)); A.bnd = (const long long *)p;
+    TRY(up(gbuf, (size_t)n_gbuf * 8, &p)); A.gbuf = (long long *)p;
+    TRY(up(g_off, gw, &p)); A.g_off = (const long long *)p;
+    TRY(up(g_cap, gw, &p)); A.g_cap = (const long long *)p;
+    TRY(up(g_cnt, gw, &p)); A.g_cnt = (long long *)p;
+    TRY(up(out_filt, gw, &p)); A.out_filt = (long long *)p;
+    TRY(up(out_icf, gw, &p)); A.out_icf = (long long *)p;
+    TRY(up(out_disc, gw, &p)); A.out_disc = (long long *)p;
+    TRY(up(out_err, gw, &p)); A.out_err = (long long *)p;
+    TRY(up(out_peak, gw, &p)); A.out_peak = (long long *)p;
+    const int64_t total = (oi_hi - oi_lo) * (w_hi - w_lo);
+    if (total) {
+      sim_span_seam<<<(int)std::min<int64_t>((total + 127) / 128, 148 * 32), 128>>>(A);
+      CK(cudaGetLastError());
+    }
+    struct { int64_t *h; void *d; size_t n; } back[] = {
+        {gbuf, A.gbuf, (size_t)n_gbuf * 8}, {g_cnt, A.g_cnt, gw}, {out_filt, A.out_filt, gw},
+        {out_icf, A.out_icf, gw}, {out_disc, A.out_disc, gw}, {out_err, A.out_err, gw},
+        {out_peak, A.out_peak, gw}};
+    for (auto &b : back)
+      if (b.n) CK(cudaMemcpy(b.h, b.d, b.n, cudaMemcpyDeviceToHost));
+    return GS_OK;
+  }();
+  for (void *b : bufs) cudaFree(b);
   return rc;
 }
 

@@ -1506,6 +1506,124 @@ __global__ void dwell_arena(DwellArgs A) {
   }
 }
 
+// ------------------------------------------------------------------- K3
+// The sim_span seam (_kernels.py:17-210) on the reference's own data layout:
+// int64 absolute times, per-(net, window) offset / count arrays, the output
+// regions g_off / g_cap of gbuf.  Thread per (gate order[oi], window w), each
+// running Algo. 1 exactly as sim_span does; for code that drives the
+// reference's per-level loop itself (the engine's path keeps its own layout).
+struct SpanArgs {
+  long long oi_lo, oi_hi, w_lo, w_hi, w_off;
+  const long long *order, *pin_off, *pin_net, *pin_ic, *pin_arc, *arc_rows, *lut_off;
+  const unsigned char *lut_bits, *net_kind;
+  const long long *net_slot, *stim_buf, *stim_off, *stim_cnt;
+  long long stim_cols;
+  const unsigned char *init_vals;
+  long long init_cols;
+  const long long *bnd;
+  long long *gbuf;
+  const long long *g_off, *g_cap;
+  long long *g_cnt;
+  long long g_cols;
+  long long *out_filt, *out_icf, *out_disc, *out_err, *out_peak;
+  long long pct;
+};
+
+__global__ void sim_span_seam(SpanArgs A) {
+  const long long Ws = A.w_hi - A.w_lo;
+  const long long total = (A.oi_hi - A.oi_lo) * Ws;
+  for (long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x; it < total;
+       it += (long long)gridDim.x * blockDim.x) {
+    const long long g = A.order[A.oi_lo + it / Ws];
+    const long long w = A.w_lo + it % Ws, wj = w - A.w_off;
+    const long long p0 = A.pin_off[g], k = A.pin_off[g + 1] - p0;
+    const long long lidx = A.lut_off[g], wend = A.bnd[w + 1];
+    long long pos[kMaxK], nxt[kMaxK], sof[kMaxK], scn[kMaxK];
+    unsigned char sst[kMaxK];
+    long long idx = 0;
+    for (long long p = 0; p < k; ++p) {
+      const long long n = A.pin_net[p0 + p], sl = A.net_slot[n];
+      sst[p] = A.net_kind[n] == 0;
+      sof[p] = sst[p] ? A.stim_off[sl * A.stim_cols + w] : A.g_off[sl * A.g_cols + wj];
+      scn[p] = sst[p] ? A.stim_cnt[sl * A.stim_cols + w] : A.g_cnt[sl * A.g_cols + wj];
+      pos[p] = 0;
+      nxt[p] = -1;  // refresh
+      if (A.init_vals[n * A.init_cols + w]) idx |= 1ll << p;
+    }
+    unsigned y = A.lut_bits[lidx + idx];
+    long long cnt = 0, peak = 0, filt = 0, icf = 0, disc = 0, t_last = 0;
+    bool has_last = false, last_stored = false, err = false;
+    const long long roff = A.g_off[g * A.g_cols + wj], rcap = A.g_cap[g * A.g_cols + wj];
+    auto store = [&](long long t) {
+      if (cnt < rcap) A.gbuf[roff + cnt] = t;
+      else err = true;
+      ++cnt;
+      peak = max(peak, cnt);
+    };
+    while (true) {
+      long long tmin = kInf;
+      for (long long p = 0; p < k; ++p) {
+        if (nxt[p] == -1) {  // next surviving arrival, narrow pairs dropped
+          const long long d = A.pin_ic[p0 + p];
+          const long long *src = sst[p] ? A.stim_buf : A.gbuf;
+          while (pos[p] + 1 < scn[p] && src[sof[p] + pos[p] + 1] - src[sof[p] + pos[p]] < d) {
+            pos[p] += 2;
+            ++icf;
+          }
+          nxt[p] = pos[p] < scn[p] ? src[sof[p] + pos[p]] + d : kInf;
+        }
+        tmin = min(tmin, nxt[p]);
+      }
+      if (tmin == kInf) break;
+      long long sw = 0;
+      for (long long p = 0; p < k; ++p)
+        if (nxt[p] == tmin) {
+          ++pos[p];
+          nxt[p] = -1;
+          idx ^= 1ll << p;
+          sw |= 1ll << p;
+        }
+      const unsigned ny = A.lut_bits[lidx + idx];
+      if (ny == y) continue;
+      const int col = ny ? 0 : 1;
+      long long dly = 0;
+      for (long long p = 0; p < k; ++p)
+        if ((sw >> p) & 1) {
+          // condition row: the other pins' post-transition values, ascending
+          const long long row = (idx & ((1ll << p) - 1)) | ((idx >> (p + 1)) << p);
+          dly = max(dly, A.arc_rows[(A.pin_arc[p0 + p] + row) * 2 + col]);
+        }
+      const long long t_out = tmin + dly, thr = dly * A.pct / 100;
+      const bool have = has_last || cnt > 0;
+      const long long tgt = has_last ? t_last : (cnt > 0 ? A.gbuf[roff + cnt - 1] : 0);
+      if (have && (t_out <= tgt || t_out - tgt < thr)) {
+        if (has_last) {
+          if (!last_stored) --disc;
+          has_last = false;
+        } else {
+          --cnt;
+        }
+        ++filt;
+      } else {
+        if (has_last && last_stored) store(t_last);
+        last_stored = t_out < wend;
+        if (!last_stored) ++disc;
+        has_last = true;
+        t_last = t_out;
+      }
+      y = ny;
+    }
+    if (has_last && last_stored) store(t_last);
+    const long long o = g * A.g_cols + wj;
+    A.g_cnt[o] = cnt;
+    A.out_filt[o] = filt;
+    A.out_icf[o] = icf;
+    A.out_disc[o] = disc;
+    A.out_peak[o] = peak;
+    if (err) A.out_err[o] = 1;
+  }
+}
+
 // ------------------------------------------------------------------- K2
 // init_values (_kernels.py:213-231) for one level: vals[P+g][w] = lut[idx].
 __global__ void zero_delay_level(DesignDev D, unsigned char *vals, long long W, int lo, int n) {

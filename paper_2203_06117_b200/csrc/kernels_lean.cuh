@@ -65,7 +65,10 @@ struct alignas(16) LeanWarp {
 
 template <int K>
 struct LeanShared {
-  unsigned short list[2][kPool];             // worklists of a step: [0] loop, [1] two
+  // worklists of a step: [0, kPool) loop windows, [kPool, 2 kPool) two-
+  // transition windows, then one sink slot per thread for the stores of
+  // lanes with no entry
+  unsigned short list[2 * kPool + kEvalThreads];
   unsigned arcs[K * (1 << (K - 1)) * 2];
   unsigned dtab[K <= 2 ? (1 << (2 * K)) * 2 : K * (1 << K) * 2];
   unsigned nlist[2][2];                      // list lengths, double-buffered by step parity
@@ -602,12 +605,16 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         }
         base = __shfl_sync(0xffffffffu, base, 0);
         unsigned xl = base & 0xFFFFu, xt = kPool + (base >> 16);
-        unsigned short *lists = &S.s.list[0][0];
+        // every lane stores each j (no branch): lanes without an entry at j
+        // write their own sink slot
+        unsigned short *lists = S.s.list;
+        const unsigned sink = 2 * kPool + (unsigned)tid;
 #pragma unroll
         for (int j = 0; j < kWPL; ++j) {
           const bool inl = (bl[j] >> lane) & 1u, intw = (bt[j] >> lane) & 1u;
-          const unsigned at = inl ? xl + __popc(bl[j] & lt) : xt + __popc(bt[j] & lt);
-          if (inl || intw) lists[at] = wl_entry(wl + j, ix[j], warp);
+          const unsigned at = inl ? xl + __popc(bl[j] & lt)
+                            : intw ? xt + __popc(bt[j] & lt) : sink;
+          lists[at] = wl_entry(wl + j, ix[j], warp);
           xl += __popc(bl[j]);
           xt += __popc(bt[j]);
         }
@@ -674,23 +681,23 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         // long event loops are spread instead of packed into one warp
         (void)L;
         for (unsigned i = lane * kEvalWarps + warp; i < nl; i += kEvalThreads) {
-          const unsigned e = S.s.list[0][i];
+          const unsigned e = S.s.list[i];
           loop_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
                                              (int)(e & 127u), (e >> 7) & 15u, acc);
         }
         for (unsigned i = tid; i < n2; i += kEvalThreads) {
-          const unsigned e = S.s.list[1][i];
+          const unsigned e = S.s.list[kPool + i];
           two_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
                                             (int)(e & 127u), (e >> 7) & 15u, acc);
         }
 #else
         for (unsigned i = tid; i < L + n2; i += kEvalThreads) {
           if (i < nl) {
-            const unsigned e = S.s.list[0][i];
+            const unsigned e = S.s.list[i];
             loop_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
                                                (int)(e & 127u), (e >> 7) & 15u, acc);
           } else if (i >= L) {
-            const unsigned e = S.s.list[1][i - L];
+            const unsigned e = S.s.list[kPool + i - L];
             two_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
                                               (int)(e & 127u), (e >> 7) & 15u, acc);
           }
