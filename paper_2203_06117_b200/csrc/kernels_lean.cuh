@@ -63,15 +63,23 @@ struct alignas(16) LeanWarp {
   unsigned long long mbar;                   // bulk-copy completion
 };
 
+// worklist classes of a window (by its input transitions); list c occupies
+// [kListAt[c], kListAt[c] + kPool) of LeanShared::list
+enum LeanClass : unsigned { kQuiet = 0, kSingle = 1, kTwo = 2, kLoop = 3 };
+constexpr unsigned kListBits = 10;                 // per-class field of a packed count
+constexpr unsigned kListMask = (1u << kListBits) - 1u;
+
 template <int K>
 struct LeanShared {
-  // worklists of a step: [0, kPool) loop windows, [kPool, 2 kPool) two-
-  // transition windows, then one sink slot per thread for the stores of
-  // lanes with no entry
-  unsigned short list[2 * kPool + kEvalThreads];
+  // worklists of a step, one region of kPool entries per class: loop
+  // windows at 0, two-transition windows at kPool, single-transition windows
+  // at 2 kPool; then one sink slot per thread for the stores of windows that
+  // need no list
+  unsigned short list[3 * kPool + kEvalThreads];
   unsigned arcs[K * (1 << (K - 1)) * 2];
   unsigned dtab[K <= 2 ? (1 << (2 * K)) * 2 : K * (1 << K) * 2];
-  unsigned nlist[2][2];                      // list lengths, double-buffered by step parity
+  unsigned nlist[2];                         // packed list lengths (single | two << 10 |
+                                             // loop << 20), double-buffered by step parity
   unsigned item;
 };
 
@@ -351,6 +359,50 @@ __device__ __forceinline__ void loop_window(const ChunkDev &C, int g, unsigned l
                                (unsigned long long)(stage + so - reinterpret_cast<unsigned *>(C.data)));
 }
 
+// One input transition: Algo. 1 with a single event (K:94-203, one
+// iteration) -- one LUT lookup, one delay lookup, one window-end test.  Only
+// staged tiles classify windows as single.
+template <int MODE, int K, bool PCT100, int SLAB>
+__device__ __forceinline__ void single_window(const ChunkDev &C, int g, unsigned long long lut,
+                                              const unsigned (&ic)[K], const unsigned *dtab,
+                                              LeanWarp<K, SLAB> &T, int w, unsigned i0,
+                                              LeanAcc &acc) {
+  unsigned *stage = reinterpret_cast<unsigned *>(T.stage);
+  const int base_w = T.t * kTile;
+  unsigned so = 0, pj = 0, at = 0, icp = ic[0];
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    const unsigned a = T.offs[p][w], m = T.offs[p][w + 1] - a;
+    so += a;
+    if (K > 1) {
+      pj = m ? (unsigned)p : pj;
+      icp = m ? ic[p] : icp;
+    }
+    at = m ? T.seg[p] + a : at;
+  }
+  const unsigned tv = T.slab[at];
+  const unsigned y0 = (unsigned)(lut >> i0) & 1u;
+  const unsigned i1 = i0 ^ (1u << pj);
+  const unsigned y1 = (unsigned)(lut >> i1) & 1u;
+  const bool chg = y1 != y0;
+  const unsigned ot = tv + icp + dtab_pin<K>(dtab, pj, i1, y1 ? 0u : 1u);
+  const unsigned wln = __ldg(C.wlen32 + base_w + w);
+  const bool inwin = ot < wln;
+  const bool st = chg && inwin;
+  if (st) stage[so] = ot;
+  const int disc = (chg && !inwin) ? 1 : 0;
+  acc.disc += disc;
+  // dwell at 1: the start value holds until the stored edge (or the window
+  // end), the other value after it
+  const unsigned e = st ? ot : wln;
+  acc.t1 += y0 ? e : wln - e;
+  T.cnt[w] = st ? 1u : 0u;
+  if (MODE != MODE_STATS)
+    record_arena<MODE, unsigned>(C, g, base_w + w, st ? 1 : 0, st ? 1 : 0, 0, 0, disc, y0,
+                                 [&](int) -> unsigned & { return stage[so]; },
+                                 (unsigned long long)(stage + so - reinterpret_cast<unsigned *>(C.data)));
+}
+
 // Two input transitions in closed form.  With no edge pending at the first
 // event, Algo. 1's output side (K:136-203) collapses to selects: event 1 (both
 // pins when the two transitions coincide) can only emit; event 2 can emit,
@@ -451,7 +503,7 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
   LeanWarp<K, SLAB> &T = S.w[warp];
   Region R = region_open(C, (unsigned long long)blockIdx.x * kEvalWarps + warp);
   if (lane == 0) mbar_init(&T.mbar, 1);
-  if (tid < 4) (&S.s.nlist[0][0])[tid] = 0;
+  if (tid < 2) S.s.nlist[tid] = 0;
   unsigned phase = 0, par = 0;
   unsigned *data = reinterpret_cast<unsigned *>(C.data);
   const int Tw = C.Wpad / 32;
@@ -512,9 +564,9 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         __syncwarp();
         // the next tile of this warp in the item: its rows fly during this one
         if (t + kSuper < t_end) prefetch_tile<K, SLAB>(C, net, t + kSuper, T);
-        unsigned n[kWPL], sidx[kWPL], sso[kWPL], ix[kWPL], p1[kWPL];
+        unsigned n[kWPL], ix[kWPL];
 #pragma unroll
-        for (int j = 0; j < kWPL; ++j) n[j] = sidx[j] = sso[j] = ix[j] = p1[j] = 0;
+        for (int j = 0; j < kWPL; ++j) n[j] = ix[j] = 0;
         unsigned tot[K], seg[K], inw = 0, UB = 0;
 #pragma unroll
         for (int p = 0; p < K; ++p) {
@@ -530,11 +582,6 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
 #pragma unroll
           for (int j = 0; j < kWPL; ++j) {
             o4[j] = ex;
-            // a one-transition window's single toggle (exactly one pin has
-            // c = 1 there): its slab slot and pin, as sums over the pins
-            sidx[j] += c[p][j] * (seg[p] + ex);
-            if (p) p1[j] += c[p][j] * (unsigned)p;
-            sso[j] += ex;
             n[j] += c[p][j];
             ix[j] |= ((bits[p] >> j) & 1u) << p;
             ex += c[p][j];
@@ -581,128 +628,93 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
             T.tb[p] = tb[p];
           }
         }
-        // worklists: two transitions, and three or more (any when in place);
-        // positions by warp ballots, one shared-memory atomic per list
-        unsigned amask = 0;  // the lane's windows inside the chunk
-#pragma unroll
-        for (int j = 0; j < kWPL; ++j) amask |= (ok && wl + j < nact ? 1u : 0u) << j;
-        const unsigned lim = in_smem ? 1u : 0u;  // windows with n <= lim finish inline
-        const unsigned lt = (1u << lane) - 1u;
-        unsigned bl[kWPL], bt[kWPL], nL = 0, nT = 0;
+        // worklists by class: staged tiles send windows with one, two, or
+        // three and more transitions to the single / two / loop lists; tiles
+        // read in place send every window with a transition to the loop list.
+        // Positions: one warp scan of the lane's packed class counts, one
+        // shared-memory atomic for all three lists of the warp.
+        unsigned cls[kWPL], V = 0;
 #pragma unroll
         for (int j = 0; j < kWPL; ++j) {
-          const bool a = (amask >> j) & 1u;
-          bl[j] = __ballot_sync(0xffffffffu, a && n[j] > lim && (n[j] > 2 || !in_smem));
-          bt[j] = __ballot_sync(0xffffffffu, a && in_smem && n[j] == 2);
-          nL += __popc(bl[j]);
-          nT += __popc(bt[j]);
+          const bool a = ok && wl + j < nact;
+          const unsigned m = in_smem ? min(n[j], 3u) : (n[j] ? 3u : 0u);
+          cls[j] = a ? m : 0u;
+          V += (1u << (kListBits * cls[j])) >> kListBits;
         }
+        unsigned VT;
+        unsigned P = warp_excl_scan(V, &VT);
         unsigned base = 0;
-        if (lane == 0) {
-          const unsigned b0 = nL ? atomicAdd(&S.s.nlist[par][0], nL) : 0u;
-          const unsigned b1 = nT ? atomicAdd(&S.s.nlist[par][1], nT) : 0u;
-          base = b0 | (b1 << 16);
-        }
-        base = __shfl_sync(0xffffffffu, base, 0);
-        unsigned xl = base & 0xFFFFu, xt = kPool + (base >> 16);
-        // every lane stores each j (no branch): lanes without an entry at j
-        // write their own sink slot
+        if (lane == 0 && VT) base = atomicAdd(&S.s.nlist[par], VT);
+        P += __shfl_sync(0xffffffffu, base, 0);
+        // every window stores (no branch): quiet ones into the thread's sink slot
         unsigned short *lists = S.s.list;
-        const unsigned sink = 2 * kPool + (unsigned)tid;
+        const unsigned sink = 3 * kPool + (unsigned)tid;
 #pragma unroll
         for (int j = 0; j < kWPL; ++j) {
-          const bool inl = (bl[j] >> lane) & 1u, intw = (bt[j] >> lane) & 1u;
-          const unsigned at = inl ? xl + __popc(bl[j] & lt)
-                            : intw ? xt + __popc(bt[j] & lt) : sink;
+          const unsigned c1 = cls[j] ? cls[j] - 1u : 0u;
+          const unsigned at = cls[j] ? (2u - c1) * kPool + ((P >> (kListBits * c1)) & kListMask)
+                                     : sink;
           lists[at] = wl_entry(wl + j, ix[j], warp);
-          xl += __popc(bl[j]);
-          xt += __popc(bt[j]);
+          P += (1u << (kListBits * cls[j])) >> kListBits;
         }
         // the staged segments have landed (all lanes observe the barrier)
         if (in_smem && inw) {
           mbar_wait(&T.mbar, phase);
           phase ^= 1u;
         }
-        // windows with no transition or one: finished here
-        unsigned oc[kWPL], wl4[kWPL];
+        // windows with no transition: the output keeps its start value
+        unsigned wl4[kWPL];
         load_counts(C.wlen32 + base_w + wl, wl4);
 #pragma unroll
         for (int j = 0; j < kWPL; ++j) {
-          const bool act = (amask >> j) & 1u;
-          const bool one = in_smem && n[j] == 1;
-          const unsigned pj = one ? p1[j] : 0u;
-          const unsigned tv = one ? T.slab[one ? sidx[j] : 0u] : 0u;
-          unsigned icp = ic[0];
-#pragma unroll
-          for (int p = 1; p < K; ++p) icp = pj == (unsigned)p ? ic[p] : icp;
+          const bool act = ok && wl + j < nact;
           const unsigned y0 = (unsigned)(lut >> ix[j]) & 1u;
-          const unsigned i1 = ix[j] ^ (1u << pj);
-          const unsigned y1 = (unsigned)(lut >> i1) & 1u;
-          const bool chg = one && y1 != y0;
-          const unsigned ot = tv + icp + dtab_pin<K>(S.s.dtab, pj, i1, y1 ? 0u : 1u);
-          const unsigned wln = wl4[j];
-          const bool inwin = ot < wln;
-          const bool st = chg && inwin;
-          const bool inl = act && n[j] <= lim;
-          // (singles occur on staged tiles only; arena runs stage outputs in the pool)
-          if (st) {
-            if (MODE == MODE_STATS) T.slab[inw + sso[j]] = ot;
-            else stage[sso[j]] = ot;
-          }
-          acc.disc += (chg && !inwin) ? 1 : 0;
-          // dwell at 1: the start value holds until the stored edge (or the
-          // window end), the other value after it
-          const unsigned e = st ? ot : wln;
-          const unsigned dw = y0 ? e : wln - e;
-          acc.t1 += inl ? dw : 0u;
+          const bool quiet = act && n[j] == 0;
+          acc.t1 += (quiet && y0) ? wl4[j] : 0u;
           nib |= (act ? y0 : 0u) << j;
-          if (MODE != MODE_STATS && inl)
-            record_arena<MODE, unsigned>(C, g, base_w + wl + j, st ? 1 : 0, st ? 1 : 0, 0, 0,
-                                         (chg && !inwin) ? 1 : 0, y0,
-                                         [&](int) -> unsigned & { return stage[sso[j]]; },
-                                         (unsigned long long)(stage + sso[j] - data));
-          oc[j] = inl && st ? 1u : 0u;  // worklist windows: written in (M)
+          if (MODE != MODE_STATS && quiet)
+            record_arena<MODE, unsigned>(C, g, base_w + wl + j, 0, 0, 0, 0, 0, y0,
+                                         [&](int) -> unsigned & { return stage[0]; },
+                                         (unsigned long long)(stage - data));
         }
-        // counts of the inline windows (worklist windows overwrite theirs)
-        st4(&T.cnt[wl], oc);
+        // counts of the quiet windows (list windows overwrite theirs)
+        const unsigned z4[kWPL] = {0u, 0u, 0u, 0u};
+        st4(&T.cnt[wl], z4);
       }
       GS_PROF_T(pt1);
       GS_PROF_ADD(PF_PHASE1, pt1 - pt0);
       __syncthreads();
-      // ---- (M) the pooled worklists of the CTA's tiles
+      // ---- (M) the pooled worklists of the CTA's tiles: loop windows first
+      // (the longest), then two-transition, then single-transition windows,
+      // each list starting on a warp boundary
       {
-        const unsigned nl = S.s.nlist[par][0], n2 = S.s.nlist[par][1];
-        if (tid < 2) S.s.nlist[par ^ 1u][tid] = 0;  // the next step's lists
-        const unsigned L = (nl + kWarp - 1) & ~(unsigned)(kWarp - 1);
-        GS_PROF_ADD(PF_LOOP_WINDOWS, warp == 0 ? nl : 0);
-        GS_PROF_ADD(PF_TRIVIAL, warp == 0 ? n2 : 0);
-#ifdef GS_LEAN_MSPREAD
-        // loop windows dealt round-robin over the warps (lane-major), so the
-        // long event loops are spread instead of packed into one warp
-        (void)L;
-        for (unsigned i = lane * kEvalWarps + warp; i < nl; i += kEvalThreads) {
-          const unsigned e = S.s.list[i];
-          loop_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
-                                             (int)(e & 127u), (e >> 7) & 15u, acc);
-        }
-        for (unsigned i = tid; i < n2; i += kEvalThreads) {
-          const unsigned e = S.s.list[kPool + i];
-          two_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
-                                            (int)(e & 127u), (e >> 7) & 15u, acc);
-        }
-#else
-        for (unsigned i = tid; i < L + n2; i += kEvalThreads) {
-          if (i < nl) {
-            const unsigned e = S.s.list[i];
-            loop_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
-                                               (int)(e & 127u), (e >> 7) & 15u, acc);
-          } else if (i >= L) {
-            const unsigned e = S.s.list[kPool + i - L];
-            two_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
-                                              (int)(e & 127u), (e >> 7) & 15u, acc);
+        const unsigned pk = S.s.nlist[par];
+        if (tid == 0) S.s.nlist[par ^ 1u] = 0;  // the next step's lists
+        const unsigned nS = pk & kListMask, nT = (pk >> kListBits) & kListMask,
+                       nL = pk >> (2 * kListBits);
+        const unsigned aL = (nL + kWarp - 1) & ~(unsigned)(kWarp - 1);
+        const unsigned aT = aL + ((nT + kWarp - 1) & ~(unsigned)(kWarp - 1));
+        GS_PROF_ADD(PF_LOOP_WINDOWS, warp == 0 ? nL : 0);
+        GS_PROF_ADD(PF_TRIVIAL, warp == 0 ? nT : 0);
+        for (unsigned i = tid; i < aT + nS; i += kEvalThreads) {
+          if (i < aL) {
+            if (i < nL) {
+              const unsigned e = S.s.list[i];
+              loop_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
+                                                 (int)(e & 127u), (e >> 7) & 15u, acc);
+            }
+          } else if (i < aT) {
+            if (i - aL < nT) {
+              const unsigned e = S.s.list[kPool + i - aL];
+              two_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
+                                                (int)(e & 127u), (e >> 7) & 15u, acc);
+            }
+          } else {
+            const unsigned e = S.s.list[2 * kPool + i - aT];
+            single_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, S.s.dtab, S.w[e >> 11],
+                                                 (int)(e & 127u), (e >> 7) & 15u, acc);
           }
         }
-#endif
       }
       GS_PROF_T(pt2);
       GS_PROF_ADD(PF_LOOP, pt2 - pt1);

@@ -71,11 +71,15 @@ def test_seam_reports_overflow():
         pytest.skip("no toggles")
     caps = np.maximum(c["peak"] - 1, 0)
     G, W = caps.shape
-    offsets = port.arena_offsets(caps, d.order)
+    # each region followed by a gap the overflowing (gate, window) reads but
+    # nobody writes: sim_span reads its last stored edge at cnt - 1 >= cap,
+    # which in a packed arena is a neighbour's region (order-dependent)
+    span = c["peak"] + 1
+    offsets = port.arena_offsets(span, d.order)
     lo, hi = int(d.level_starts[0]), int(d.level_starts[1])
     runs = []
     for level in (port._sim_level, _gpu_level):
-        buf = np.full(int(caps.sum()) + 1, -7, dtype=np.int64)
+        buf = np.full(int(span.sum()), -7, dtype=np.int64)
         z = [np.zeros((G, W), dtype=np.int64) for _ in range(6)]
         counts, filt, icf, disc, err, peak = z
         level(d, st, vals, buf, offsets, caps, counts, filt, icf, disc, err, peak,
