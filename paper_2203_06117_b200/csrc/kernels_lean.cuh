@@ -57,6 +57,7 @@ struct alignas(16) LeanWarp {
   alignas(16) unsigned cnt[kTile];           // stored toggles per window
   unsigned long long tb[K];                  // in place: pin p's tile base in `data`
   unsigned long long stage;                  // generic address of the output staging area
+  unsigned stage_at;                         // ... its slab offset (staged statistics runs)
   unsigned seg[K];                           // staged: pin p's segment at slab[seg[p]]
   int t;                                     // tile index
   int in_smem;
@@ -200,13 +201,20 @@ __device__ __forceinline__ unsigned short wl_entry(int w, unsigned ix, int warp)
   return (unsigned short)((unsigned)w | (ix << 7) | ((unsigned)warp << 11));
 }
 
-// the staged-or-in-place sources of warp `wi`'s tile
-template <int K, int SLAB>
+// the sources of a tile's fanin segments: the slab (SMEM, shared-memory
+// addressing) or the segments in place
+template <bool SMEM, int K, int SLAB>
 __device__ __forceinline__ void tile_sources(const ChunkDev &C, LeanWarp<K, SLAB> &T,
                                              const unsigned *(&src)[K]) {
   unsigned *data = reinterpret_cast<unsigned *>(C.data);
 #pragma unroll
-  for (int p = 0; p < K; ++p) src[p] = T.in_smem ? &T.slab[T.seg[p]] : data + T.tb[p];
+  for (int p = 0; p < K; ++p) src[p] = SMEM ? &T.slab[T.seg[p]] : data + T.tb[p];
+}
+// a tile's output staging area (the slab for staged statistics runs)
+template <bool SMEM, int MODE, int K, int SLAB>
+__device__ __forceinline__ unsigned *tile_stage(LeanWarp<K, SLAB> &T) {
+  if (SMEM && MODE == MODE_STATS) return &T.slab[T.stage_at];
+  return reinterpret_cast<unsigned *>(T.stage);
 }
 
 // cp.async of tile t's fanin count rows (a 16-byte piece per lane), the
@@ -236,15 +244,15 @@ __device__ __forceinline__ void prefetch_tile(const ChunkDev &C, const int (&net
 // more input transitions, the interconnect pair filter applied lazily as
 // sim_span's refresh does (_kernels.py:96-117).  Outputs go to the tile's
 // staging area at the window's slot.
-template <int MODE, int K, bool PCT100, int SLAB>
+template <int MODE, int K, bool PCT100, bool SMEM, int SLAB>
 __device__ __forceinline__ void loop_window(const ChunkDev &C, int g, unsigned long long lut,
                                             const unsigned (&ic)[K], int pct,
                                             const unsigned *dtab, LeanWarp<K, SLAB> &T, int w,
                                             unsigned idx, LeanAcc &acc) {
   constexpr unsigned INF = 0xffffffffu;
   const unsigned *src[K];
-  tile_sources<K, SLAB>(C, T, src);
-  unsigned *stage = reinterpret_cast<unsigned *>(T.stage);
+  tile_sources<SMEM, K, SLAB>(C, T, src);
+  unsigned *stage = tile_stage<SMEM, MODE, K, SLAB>(T);
   const int base_w = T.t * kTile;
   unsigned cur[K], end[K], nxt[K], so = 0;
   int icf = 0;
@@ -367,7 +375,7 @@ __device__ __forceinline__ void single_window(const ChunkDev &C, int g, unsigned
                                               const unsigned (&ic)[K], const unsigned *dtab,
                                               LeanWarp<K, SLAB> &T, int w, unsigned i0,
                                               LeanAcc &acc) {
-  unsigned *stage = reinterpret_cast<unsigned *>(T.stage);
+  unsigned *stage = tile_stage<true, MODE, K, SLAB>(T);
   const int base_w = T.t * kTile;
   unsigned so = 0, pj = 0, at = 0, icp = ic[0];
 #pragma unroll
@@ -413,8 +421,8 @@ __device__ __forceinline__ void two_window(const ChunkDev &C, int g, unsigned lo
                                            const unsigned *dtab, LeanWarp<K, SLAB> &T, int w,
                                            unsigned i0, LeanAcc &acc) {
   const unsigned *src[K];
-  tile_sources<K, SLAB>(C, T, src);
-  unsigned *stage = reinterpret_cast<unsigned *>(T.stage);
+  tile_sources<true, K, SLAB>(C, T, src);  // two-transition windows come from staged tiles
+  unsigned *stage = tile_stage<true, MODE, K, SLAB>(T);
   const int base_w = T.t * kTile;
   unsigned nt = 0, pa = 0, pb = 0, so = 0;
   const unsigned *qa = src[0], *qb = src[0];
@@ -564,16 +572,59 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         __syncwarp();
         // the next tile of this warp in the item: its rows fly during this one
         if (t + kSuper < t_end) prefetch_tile<K, SLAB>(C, net, t + kSuper, T);
+        // window-start input vectors: the (pin x window) bit matrix transposed
         unsigned n[kWPL], ix[kWPL];
+        {
+          unsigned B = 0;
 #pragma unroll
-        for (int j = 0; j < kWPL; ++j) n[j] = ix[j] = 0;
-        unsigned tot[K], seg[K], inw = 0, UB = 0;
+          for (int p = 0; p < K; ++p) B |= bits[p] << (4 * p);
+          if (K > 1) {
+            unsigned x = (B ^ (B >> 3)) & 0x0A0Au;
+            B ^= x ^ (x << 3);
+            x = (B ^ (B >> 6)) & 0x00CCu;
+            B ^= x ^ (x << 6);
+          }
+#pragma unroll
+          for (int j = 0; j < kWPL; ++j) {
+            ix[j] = K > 1 ? (B >> (4 * j)) & 15u : (B >> j) & 1u;
+            n[j] = 0;
+          }
+        }
+        // per-pin window offsets: warp scans of the lane sums, two pins per
+        // scan (16-bit halves) unless some lane's sum could overflow a half
+        unsigned s4[K], ex0[K], tot[K];
 #pragma unroll
         for (int p = 0; p < K; ++p) {
-          unsigned s4 = 0;
+          s4[p] = 0;
 #pragma unroll
-          for (int j = 0; j < kWPL; ++j) s4 += c[p][j];
-          unsigned ex = warp_excl_scan(s4, &tot[p]);
+          for (int j = 0; j < kWPL; ++j) s4[p] += c[p][j];
+        }
+        bool pair = false;
+        if constexpr (K > 1) {
+          unsigned big = 0;
+#pragma unroll
+          for (int p = 0; p < K; ++p) big |= s4[p];
+          pair = !__any_sync(0xffffffffu, big >= 2048u);
+        }
+        if (pair) {
+#pragma unroll
+          for (int p = 0; p + 1 < K; p += 2) {
+            unsigned t2;
+            const unsigned e = warp_excl_scan(s4[p] | (s4[p + 1] << 16), &t2);
+            ex0[p] = e & 0xFFFFu;
+            ex0[p + 1] = e >> 16;
+            tot[p] = t2 & 0xFFFFu;
+            tot[p + 1] = t2 >> 16;
+          }
+          if (K & 1) ex0[K - 1] = warp_excl_scan(s4[K - 1], &tot[K - 1]);
+        } else {
+#pragma unroll
+          for (int p = 0; p < K; ++p) ex0[p] = warp_excl_scan(s4[p], &tot[p]);
+        }
+        unsigned seg[K], inw = 0, UB = 0;
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          unsigned ex = ex0[p];
           const unsigned sh = (unsigned)tb[p] & 3u;
           seg[p] = inw + sh;
           inw += tot[p] ? (sh + tot[p] + 3u) & ~3u : 0u;
@@ -583,7 +634,6 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
           for (int j = 0; j < kWPL; ++j) {
             o4[j] = ex;
             n[j] += c[p][j];
-            ix[j] |= ((bits[p] >> j) & 1u) << p;
             ex += c[p][j];
           }
           st4(&T.offs[p][wl], o4);
@@ -622,6 +672,7 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
           T.in_smem = in_smem ? 1 : 0;
           T.t = t;
           T.stage = reinterpret_cast<unsigned long long>(stage);
+          T.stage_at = inw;
 #pragma unroll
           for (int p = 0; p < K; ++p) {
             T.seg[p] = seg[p];
@@ -700,8 +751,13 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
           if (i < aL) {
             if (i < nL) {
               const unsigned e = S.s.list[i];
-              loop_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
-                                                 (int)(e & 127u), (e >> 7) & 15u, acc);
+              LeanWarp<K, SLAB> &Tw = S.w[e >> 11];
+              if (Tw.in_smem)
+                loop_window<MODE, K, PCT100, true, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, Tw,
+                                                         (int)(e & 127u), (e >> 7) & 15u, acc);
+              else
+                loop_window<MODE, K, PCT100, false, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, Tw,
+                                                          (int)(e & 127u), (e >> 7) & 15u, acc);
             }
           } else if (i < aT) {
             if (i - aL < nT) {
