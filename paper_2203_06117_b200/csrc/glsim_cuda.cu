@@ -526,14 +526,15 @@ namespace {
 constexpr int kMaxDevices = 64;
 
 template <typename F>
-int kernel_grid(F kernel, size_t smem, int sms, int *cache, int *grid) {
+int kernel_grid(F kernel, size_t smem, int sms, int *cache, int *grid,
+                int threads = kEvalThreads) {
   int dev = 0;
   CK(cudaGetDevice(&dev));
   if (dev < 0 || dev >= kMaxDevices) return fail(GS_ERR_ARG, "device index out of range");
   if (!cache[dev]) {
     CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kEvalThreads, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem));
     cache[dev] = std::max(1, occ);
   }
   *grid = sms * cache[dev];
@@ -550,7 +551,8 @@ int eval_grid(int sms, int *grid) {
 template <int MODE, int K, bool P100>
 int lean_grid(int sms, int *grid) {
   static int cache[kMaxDevices] = {};
-  return kernel_grid(gate_eval_lean<MODE, K, P100>, lean_smem_bytes<K>(), sms, cache, grid);
+  return kernel_grid(gate_eval_lean<MODE, K, P100>, lean_smem_bytes<K>(), sms, cache, grid,
+                     kLeanThreads);
 }
 
 template <typename TS, typename TT, int MODE, int K, bool P100>
@@ -570,7 +572,7 @@ int launch_lean(int sms, cudaStream_t st, const DesignDev &Dd, const ChunkDev &C
   int grid = 0;
   TRY((lean_grid<MODE, K, P100>(sms, &grid)));
   grid = std::min(grid, max_grid);
-  gate_eval_lean<MODE, K, P100><<<grid, kEvalThreads, lean_smem_bytes<K>(), st>>>(Dd, C, A);
+  gate_eval_lean<MODE, K, P100><<<grid, kLeanThreads, lean_smem_bytes<K>(), st>>>(Dd, C, A);
   CK(cudaGetLastError());
   return GS_OK;
 }
@@ -761,7 +763,7 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
   const bool p100 = pct == 100;
   int ncta = 0;
   TRY((grid_size<TS, MODE>(e, narrow, p100, &ncta)));
-  const int nregions = ncta * kEvalWarps;
+  const int nregions = ncta * std::max(kEvalWarps, kLeanWarps);
   if (nregions > e->ncta_cap) {
     dfree(e->bump);
     TRY(dalloc(&e->bump, 2 * (size_t)nregions + 1));  // slot states + block counter

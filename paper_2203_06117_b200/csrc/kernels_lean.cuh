@@ -34,14 +34,22 @@
 
 namespace gs {
 
-// CTAs of 4 warps per SM each fixed-K instance is built for (launch bounds)
+#ifndef GS_LEAN_WARPS
+#define GS_LEAN_WARPS 4   // warps per CTA (dev A/B knob)
+#endif
+// CTAs per SM each fixed-K instance is built for (launch bounds), given as
+// the count of 4-warp CTAs
 #ifndef GS_LEAN_CTAS2
 #define GS_LEAN_CTAS2 8   // CTAs per SM of the k <= 2 instances (dev A/B knob)
 #endif
 template <int K>
-__host__ __device__ constexpr int lean_ctas() { return K <= 2 ? GS_LEAN_CTAS2 : K == 3 ? 7 : 6; }
+__host__ __device__ constexpr int lean_ctas() {
+  return (K <= 2 ? GS_LEAN_CTAS2 : K == 3 ? 7 : 6) * 4 / GS_LEAN_WARPS;
+}
 
-constexpr int kSuper = kEvalWarps;         // tiles per CTA step (one per warp)
+constexpr int kLeanWarps = GS_LEAN_WARPS;
+constexpr int kLeanThreads = kLeanWarps * kWarp;
+constexpr int kSuper = kLeanWarps;         // tiles per CTA step (one per warp)
 constexpr int kPool = kSuper * kTile;      // windows per CTA step
 
 // per-warp part: staged segments and tile state
@@ -76,7 +84,7 @@ struct LeanShared {
   // windows at 0, two-transition windows at kPool, single-transition windows
   // at 2 kPool; then one sink slot per thread for the stores of windows that
   // need no list
-  unsigned short list[3 * kPool + kEvalThreads];
+  unsigned short list[3 * kPool + kLeanThreads];
   unsigned arcs[K * (1 << (K - 1)) * 2];
   unsigned dtab[K <= 2 ? (1 << (2 * K)) * 2 : K * (1 << K) * 2];
   unsigned nlist[2];                         // packed list lengths (single | two << 10 |
@@ -88,13 +96,13 @@ struct LeanShared {
 // (1 KB per CTA reserved)
 template <int K>
 __host__ __device__ constexpr int lean_slab_words() {
-  return (int)(((233472 / lean_ctas<K>() - 1024 - sizeof(LeanShared<K>) - 64) / kEvalWarps -
+  return (int)(((233472 / lean_ctas<K>() - 1024 - sizeof(LeanShared<K>) - 64) / kLeanWarps -
                 sizeof(LeanWarp<K, 4>) + 16) / 16 * 4);
 }
 
 template <int K>
 struct alignas(16) LeanSmem {
-  LeanWarp<K, lean_slab_words<K>()> w[kEvalWarps];
+  LeanWarp<K, lean_slab_words<K>()> w[kLeanWarps];
   LeanShared<K> s;
 };
 
@@ -499,7 +507,7 @@ __device__ __forceinline__ void two_window(const ChunkDev &C, int g, unsigned lo
 // fanin tiles while they are in L2), head items of tpi super-tiles then tail
 // items of tpi2.
 template <int MODE, int K, bool PCT100>
-__global__ void __launch_bounds__(kEvalThreads, lean_ctas<K>())
+__global__ void __launch_bounds__(kLeanThreads, lean_ctas<K>())
 gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
   constexpr int SLAB = lean_slab_words<K>();
   using SM = LeanSmem<K>;
@@ -509,7 +517,7 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
   const int tid = threadIdx.x;
   const unsigned lane = lane_id();
   LeanWarp<K, SLAB> &T = S.w[warp];
-  Region R = region_open(C, (unsigned long long)blockIdx.x * kEvalWarps + warp);
+  Region R = region_open(C, (unsigned long long)blockIdx.x * kLeanWarps + warp);
   if (lane == 0) mbar_init(&T.mbar, 1);
   if (tid < 2) S.s.nlist[tid] = 0;
   unsigned phase = 0, par = 0;
@@ -747,7 +755,7 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         const unsigned aT = aL + ((nT + kWarp - 1) & ~(unsigned)(kWarp - 1));
         GS_PROF_ADD(PF_LOOP_WINDOWS, warp == 0 ? nL : 0);
         GS_PROF_ADD(PF_TRIVIAL, warp == 0 ? nT : 0);
-        for (unsigned i = tid; i < aT + nS; i += kEvalThreads) {
+        for (unsigned i = tid; i < aT + nS; i += kLeanThreads) {
           if (i < aL) {
             if (i < nL) {
               const unsigned e = S.s.list[i];
