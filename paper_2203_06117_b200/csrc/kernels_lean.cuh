@@ -86,6 +86,7 @@ struct LeanShared {
   // need no list
   unsigned short list[3 * kPool + kLeanThreads];
   unsigned arcs[K * (1 << (K - 1)) * 2];
+  unsigned ic[K];                            // the gate's interconnect delays, by pin
   unsigned dtab[K <= 2 ? (1 << (2 * K)) * 2 : K * (1 << K) * 2];
   unsigned nlist[2];                         // packed list lengths (single | two << 10 |
                                              // loop << 20), double-buffered by step parity
@@ -258,8 +259,11 @@ __device__ __forceinline__ void loop_window(const ChunkDev &C, int g, unsigned l
                                             const unsigned *dtab, LeanWarp<K, SLAB> &T, int w,
                                             unsigned idx, LeanAcc &acc) {
   constexpr unsigned INF = 0xffffffffu;
+  // staged: cursors are absolute slab indices (one base for every pin);
+  // in place: per-pin segment pointers and relative cursors
   const unsigned *src[K];
   tile_sources<SMEM, K, SLAB>(C, T, src);
+  auto at = [&](int p, unsigned q) -> unsigned { return SMEM ? T.slab[q] : src[p][q]; };
   unsigned *stage = tile_stage<SMEM, MODE, K, SLAB>(T);
   const int base_w = T.t * kTile;
   unsigned cur[K], end[K], nxt[K], so = 0;
@@ -268,19 +272,21 @@ __device__ __forceinline__ void loop_window(const ChunkDev &C, int g, unsigned l
     unsigned q = cur[p];
     const unsigned d = ic[p];
     if (d > 0) {
-      while (q + 1 < end[p] && src[p][q + 1] - src[p][q] < d) {
+      while (q + 1 < end[p] && at(p, q + 1) - at(p, q) < d) {
         q += 2;
         ++icf;
       }
       cur[p] = q;
     }
-    nxt[p] = q < end[p] ? src[p][q] + d : INF;
+    nxt[p] = q < end[p] ? at(p, q) + d : INF;
   };
 #pragma unroll
   for (int p = 0; p < K; ++p) {
-    cur[p] = T.offs[p][w];
-    end[p] = T.offs[p][w + 1];
-    so += cur[p];
+    const unsigned a = T.offs[p][w];
+    const unsigned b0 = SMEM ? T.seg[p] : 0u;
+    cur[p] = b0 + a;
+    end[p] = b0 + T.offs[p][w + 1];
+    so += a;
     refresh(p);
   }
   const unsigned y0 = (unsigned)(lut >> idx) & 1u;
@@ -380,23 +386,23 @@ __device__ __forceinline__ void loop_window(const ChunkDev &C, int g, unsigned l
 // staged tiles classify windows as single.
 template <int MODE, int K, bool PCT100, int SLAB>
 __device__ __forceinline__ void single_window(const ChunkDev &C, int g, unsigned long long lut,
-                                              const unsigned (&ic)[K], const unsigned *dtab,
+                                              const unsigned (&ic)[K], const unsigned *ic_of,
+                                              const unsigned *dtab,
                                               LeanWarp<K, SLAB> &T, int w, unsigned i0,
                                               LeanAcc &acc) {
   unsigned *stage = tile_stage<true, MODE, K, SLAB>(T);
   const int base_w = T.t * kTile;
-  unsigned so = 0, pj = 0, at = 0, icp = ic[0];
+  // the one toggling pin: its bit in the mask of pins with a toggle
+  unsigned so = 0, mask = 0;
 #pragma unroll
   for (int p = 0; p < K; ++p) {
-    const unsigned a = T.offs[p][w], m = T.offs[p][w + 1] - a;
+    const unsigned a = T.offs[p][w];
     so += a;
-    if (K > 1) {
-      pj = m ? (unsigned)p : pj;
-      icp = m ? ic[p] : icp;
-    }
-    at = m ? T.seg[p] + a : at;
+    if (K > 1) mask |= (T.offs[p][w + 1] != a ? 1u : 0u) << p;
   }
-  const unsigned tv = T.slab[at];
+  const unsigned pj = K > 1 ? (unsigned)__ffs(mask) - 1u : 0u;
+  const unsigned icp = K > 1 ? ic_of[pj] : ic[0];
+  const unsigned tv = T.slab[T.seg[pj] + T.offs[pj][w]];
   const unsigned y0 = (unsigned)(lut >> i0) & 1u;
   const unsigned i1 = i0 ^ (1u << pj);
   const unsigned y1 = (unsigned)(lut >> i1) & 1u;
@@ -425,32 +431,29 @@ __device__ __forceinline__ void single_window(const ChunkDev &C, int g, unsigned
 // cancel event 1's edge, or leave it pending; no stored edge can be popped.
 template <int MODE, int K, bool PCT100, int SLAB>
 __device__ __forceinline__ void two_window(const ChunkDev &C, int g, unsigned long long lut,
-                                           const unsigned (&ic)[K], int pct,
-                                           const unsigned *dtab, LeanWarp<K, SLAB> &T, int w,
-                                           unsigned i0, LeanAcc &acc) {
-  const unsigned *src[K];
-  tile_sources<true, K, SLAB>(C, T, src);  // two-transition windows come from staged tiles
+                                           const unsigned (&ic)[K], const unsigned *ic_of,
+                                           int pct, const unsigned *dtab, LeanWarp<K, SLAB> &T,
+                                           int w, unsigned i0, LeanAcc &acc) {
+  // two-transition windows come from staged tiles
   unsigned *stage = tile_stage<true, MODE, K, SLAB>(T);
   const int base_w = T.t * kTile;
-  unsigned nt = 0, pa = 0, pb = 0, so = 0;
-  const unsigned *qa = src[0], *qb = src[0];
+  // the toggling pins: both toggles on one pin (dbl), or the two lowest pins
+  // of the mask of pins with a toggle
+  unsigned so = 0, mask = 0, dbl = 0;
 #pragma unroll
   for (int p = 0; p < K; ++p) {
     const unsigned a = T.offs[p][w], m = T.offs[p][w + 1] - a;
     so += a;
-    pa = (m >= 1 && nt == 0) ? (unsigned)p : pa;
-    qa = (m >= 1 && nt == 0) ? src[p] + a : qa;
-    pb = ((m >= 1 && nt == 1) || (m >= 2 && nt == 0)) ? (unsigned)p : pb;
-    qb = (m >= 1 && nt == 1) ? src[p] + a : (m >= 2 && nt == 0) ? src[p] + a + 1 : qb;
-    nt += m;
+    mask |= (m != 0 ? 1u : 0u) << p;
+    dbl |= (m >= 2 ? 1u : 0u) << p;
   }
-  unsigned ica = ic[0], icb = ic[0];
-#pragma unroll
-  for (int p = 1; p < K; ++p) {
-    ica = pa == (unsigned)p ? ic[p] : ica;
-    icb = pb == (unsigned)p ? ic[p] : icb;
-  }
-  const unsigned va = *qa, vb = *qb;
+  unsigned pa = (unsigned)__ffs(dbl ? dbl : mask) - 1u;
+  unsigned pb = dbl ? pa : (unsigned)__ffs(mask & (mask - 1u)) - 1u;
+  if (K == 1) pa = pb = 0;
+  const unsigned xa = T.seg[pa] + T.offs[pa][w];
+  const unsigned xb = dbl ? xa + 1u : T.seg[pb] + T.offs[pb][w];
+  const unsigned ica = K > 1 ? ic_of[pa] : ic[0], icb = K > 1 ? ic_of[pb] : ic[0];
+  const unsigned va = T.slab[xa], vb = T.slab[xb];
   // a same-pin pair narrower than the pin's interconnect delay is filtered
   // out whole (_kernels.py:96-117): no event remains
   const bool pairf = pa == pb && ica > 0 && vb - va < ica;
@@ -550,6 +553,12 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
       arc[p] = __ldg(D.pin_arc + pin0 + p);
     }
     if (warp == 0) build_dtab<K>(S.s.arcs, S.s.dtab, D.arc32, arc);
+    if (tid < K) {
+      unsigned v = ic[0];
+#pragma unroll
+      for (int p = 1; p < K; ++p) v = tid == p ? ic[p] : v;
+      S.s.ic[tid] = v;
+    }
     __syncthreads();
     LeanAcc acc;
     const int t_end = min(u_hi * kSuper, C.Tc);
@@ -770,12 +779,14 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
           } else if (i < aT) {
             if (i - aL < nT) {
               const unsigned e = S.s.list[kPool + i - aL];
-              two_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, S.w[e >> 11],
+              two_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, S.s.ic, A.pct, S.s.dtab,
+                                                S.w[e >> 11],
                                                 (int)(e & 127u), (e >> 7) & 15u, acc);
             }
           } else {
             const unsigned e = S.s.list[2 * kPool + i - aT];
-            single_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, S.s.dtab, S.w[e >> 11],
+            single_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, S.s.ic, S.s.dtab,
+                                                 S.w[e >> 11],
                                                  (int)(e & 127u), (e >> 7) & 15u, acc);
           }
         }
