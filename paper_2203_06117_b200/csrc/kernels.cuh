@@ -165,6 +165,21 @@ __device__ __forceinline__ T warp_excl_scan(T v, T *total) {
   return x - v;
 }
 
+// 32-bit scan: the shuffle's own in-range predicate gates each add (no
+// lane-index test)
+__device__ __forceinline__ unsigned warp_excl_scan(unsigned v, unsigned *total) {
+  unsigned x = v;
+#pragma unroll
+  for (int o = 1; o < kWarp; o <<= 1)
+    asm("{\n\t.reg .b32 y;\n\t.reg .pred p;\n\t"
+        "shfl.sync.up.b32 y|p, %0, %1, 0, -1;\n\t"
+        "@p add.u32 %0, %0, y;\n\t}"
+        : "+r"(x)
+        : "r"(o));
+  *total = __shfl_sync(0xffffffffu, x, kWarp - 1);
+  return x - v;
+}
+
 __device__ __forceinline__ long long warp_sum(long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

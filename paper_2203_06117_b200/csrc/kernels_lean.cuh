@@ -231,8 +231,7 @@ __device__ __forceinline__ unsigned *tile_stage(LeanWarp<K, SLAB> &T) {
 // warp's prefetch buffers; completed by cp.async.wait_all + __syncwarp.
 template <int K, int SLAB>
 __device__ __forceinline__ void prefetch_tile(const ChunkDev &C, const int (&net)[K], int t,
-                                              LeanWarp<K, SLAB> &T) {
-  const unsigned lane = lane_id();
+                                              LeanWarp<K, SLAB> &T, unsigned lane) {
   const int Tw = C.Wpad / 32;
 #pragma unroll
   for (int p = 0; p < K; ++p)
@@ -516,9 +515,12 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
   using SM = LeanSmem<K>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SM &S = *reinterpret_cast<SM *>(smem_raw);
-  const int warp = threadIdx.x / kWarp;
-  const int tid = threadIdx.x;
-  const unsigned lane = lane_id();
+  // the thread index through a shuffle, so that register allocation keeps it
+  // (and the warp's slice of shared memory derived from it) in registers
+  // instead of re-reading the special register at every use
+  const int tid = (int)__shfl_sync(0xffffffffu, threadIdx.x, threadIdx.x & (kWarp - 1));
+  const int warp = tid / kWarp;
+  const unsigned lane = (unsigned)tid & (kWarp - 1);
   LeanWarp<K, SLAB> &T = S.w[warp];
   Region R = region_open(C, (unsigned long long)blockIdx.x * kLeanWarps + warp);
   if (lane == 0) mbar_init(&T.mbar, 1);
@@ -562,7 +564,7 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
     __syncthreads();
     LeanAcc acc;
     const int t_end = min(u_hi * kSuper, C.Tc);
-    if (u_lo * kSuper + warp < t_end) prefetch_tile<K, SLAB>(C, net, u_lo * kSuper + warp, T);
+    if (u_lo * kSuper + warp < t_end) prefetch_tile<K, SLAB>(C, net, u_lo * kSuper + warp, T, lane);
     for (int t0 = u_lo * kSuper; t0 < t_end; t0 += kSuper, par ^= 1u) {
       const int t = t0 + warp;
       const bool tile = t < t_end;
@@ -588,7 +590,7 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         }
         __syncwarp();
         // the next tile of this warp in the item: its rows fly during this one
-        if (t + kSuper < t_end) prefetch_tile<K, SLAB>(C, net, t + kSuper, T);
+        if (t + kSuper < t_end) prefetch_tile<K, SLAB>(C, net, t + kSuper, T, lane);
         // window-start input vectors: the (pin x window) bit matrix transposed
         unsigned n[kWPL], ix[kWPL];
         {
