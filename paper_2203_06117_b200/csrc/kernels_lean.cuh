@@ -674,7 +674,9 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
                          ((sh + tot[p] + 3u) & ~3u) * 4u, &T.mbar);
               }
           }
-          stage = &T.slab[inw];
+          // staged statistics runs address the slab by offset (stage_at);
+          // no generic pointer is formed
+          stage = nullptr;
           if (MODE != MODE_STATS) {
             // arena runs: outputs stay in the pool until the chunk's arena is
             // packed (K5)
@@ -820,10 +822,10 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         const unsigned cx = warp_excl_scan(s, &CNT);
         const unsigned long long ob = CNT ? region_alloc(C, R, CNT) : 0ull;
         const bool wrote = ob != ~0ull;  // else the chunk is re-run; keep readers in bounds
-        const unsigned *stage = reinterpret_cast<const unsigned *>(T.stage);
-        if (wrote) {
-          // up to two outputs per window as predicated copies; the rare
-          // windows with more take a loop
+        // up to two outputs per window as predicated copies; the rare windows
+        // with more take a loop.  Staged statistics tiles read the slab with
+        // shared-memory addressing, the others the generic staging pointer.
+        auto copy_out = [&](const unsigned *stage) {
           unsigned *dst = data + ob + cx;
           unsigned o = 0;
           bool big = false;
@@ -843,6 +845,12 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
               o += co[j];
             }
           }
+        };
+        if (wrote) {
+          if (MODE == MODE_STATS && T.in_smem)
+            copy_out(&T.slab[T.stage_at]);
+          else
+            copy_out(reinterpret_cast<const unsigned *>(T.stage));
         }
         acc.tc += s;
         if (lane == 0) C.tbase[(size_t)gnet * C.Tc + t] = wrote ? ob : 0ull;
