@@ -303,12 +303,25 @@ __device__ __forceinline__ void loop_window(const ChunkDev &C, int g, unsigned l
 #pragma unroll
     for (int p = 0; p < K; ++p) sw |= (nxt[p] == tmin ? 1u : 0u) << p;
     idx ^= sw;
+    // the switching pins advance: predicated per pin (no divergent branch);
+    // only a narrow pair (rare) enters the filter loop
 #pragma unroll
-    for (int p = 0; p < K; ++p)
-      if ((sw >> p) & 1u) {
-        cur[p] += 1;
-        refresh(p);
+    for (int p = 0; p < K; ++p) {
+      const bool adv = (sw >> p) & 1u;
+      unsigned q = cur[p] + (adv ? 1u : 0u);
+      const unsigned d = ic[p];
+      if (d > 0) {  // the gate's pin: uniform across the CTA
+        bool narrow = adv && q + 1 < end[p] && at(p, q + 1) - at(p, q) < d;
+        while (narrow) {
+          q += 2;
+          ++icf;
+          narrow = q + 1 < end[p] && at(p, q + 1) - at(p, q) < d;
+        }
       }
+      cur[p] = q;
+      const unsigned v = adv && q < end[p] ? at(p, q) + d : INF;
+      nxt[p] = adv ? v : nxt[p];
+    }
     // output side (K:136-193)
     const unsigned ny = (unsigned)(lut >> idx) & 1u;
     const bool chg = ny != y;
@@ -768,31 +781,29 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         const unsigned aT = aL + ((nT + kWarp - 1) & ~(unsigned)(kWarp - 1));
         GS_PROF_ADD(PF_LOOP_WINDOWS, warp == 0 ? nL : 0);
         GS_PROF_ADD(PF_TRIVIAL, warp == 0 ? nT : 0);
-        for (unsigned i = tid; i < aT + nS; i += kLeanThreads) {
-          if (i < aL) {
-            if (i < nL) {
-              const unsigned e = S.s.list[i];
-              LeanWarp<K, SLAB> &Tw = S.w[e >> 11];
-              if (Tw.in_smem)
-                loop_window<MODE, K, PCT100, true, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, Tw,
-                                                         (int)(e & 127u), (e >> 7) & 15u, acc);
-              else
-                loop_window<MODE, K, PCT100, false, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, Tw,
-                                                          (int)(e & 127u), (e >> 7) & 15u, acc);
-            }
-          } else if (i < aT) {
-            if (i - aL < nT) {
-              const unsigned e = S.s.list[kPool + i - aL];
-              two_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, S.s.ic, A.pct, S.s.dtab,
-                                                S.w[e >> 11],
-                                                (int)(e & 127u), (e >> 7) & 15u, acc);
-            }
-          } else {
-            const unsigned e = S.s.list[2 * kPool + i - aT];
-            single_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, S.s.ic, S.s.dtab,
-                                                 S.w[e >> 11],
-                                                 (int)(e & 127u), (e >> 7) & 15u, acc);
-          }
+        // one index space [0, aT + nS) dealt to the threads round robin;
+        // each list walked by its own loop from the thread's first index in
+        // the list's range
+        const unsigned ut = (unsigned)tid;
+        for (unsigned i = ut; i < nL; i += kLeanThreads) {
+          const unsigned e = S.s.list[i];
+          LeanWarp<K, SLAB> &Tw = S.w[e >> 11];
+          if (Tw.in_smem)
+            loop_window<MODE, K, PCT100, true, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, Tw,
+                                                     (int)(e & 127u), (e >> 7) & 15u, acc);
+          else
+            loop_window<MODE, K, PCT100, false, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, Tw,
+                                                      (int)(e & 127u), (e >> 7) & 15u, acc);
+        }
+        for (unsigned i = aL + ((ut - aL) & (kLeanThreads - 1)); i < aL + nT; i += kLeanThreads) {
+          const unsigned e = S.s.list[kPool + i - aL];
+          two_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, S.s.ic, A.pct, S.s.dtab, S.w[e >> 11],
+                                            (int)(e & 127u), (e >> 7) & 15u, acc);
+        }
+        for (unsigned i = aT + ((ut - aT) & (kLeanThreads - 1)); i < aT + nS; i += kLeanThreads) {
+          const unsigned e = S.s.list[2 * kPool + i - aT];
+          single_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, S.s.ic, S.s.dtab, S.w[e >> 11],
+                                               (int)(e & 127u), (e >> 7) & 15u, acc);
         }
       }
       GS_PROF_T(pt2);
