@@ -33,15 +33,15 @@ EXHAUSTED = None
 
 
 # ---------------------------------------------------------------------------
-# object layer (reference SC:32-197)
+# object layer (reference SC:32-197): the names, fields and results of the
+# reference's per-gate Python model, organised around a waveform view that
+# drops narrow pairs and an output edge log
 
 @dataclass
 class PinCursor:
-    """Scan position of one input pin over its driver's window waveform.
-
-    The view is shifted by the pin's interconnect delay and filtered against
-    it: an adjacent toggle pair closer than the delay is skipped whole.
-    """
+    """One input pin's view of its driver's window waveform: every toggle
+    arrives ``ic_delay`` later, and a toggle pair closer together than
+    ``ic_delay`` never arrives (``filtered`` counts such pairs)."""
 
     times: np.ndarray
     ic_delay: int
@@ -53,13 +53,20 @@ class PinCursor:
     def from_waveform(cls, w, ic_delay=0):
         return cls(w.times, int(ic_delay), int(w.initial))
 
+    def _drop_narrow_pairs(self):
+        t, d, i = self.times, self.ic_delay, self.pos
+        while i + 1 < len(t) and t[i + 1] - t[i] < d:
+            i += 2
+        self.filtered += (i - self.pos) // 2
+        self.pos = i
+
     def peek(self):
-        """Next delayed transition time, or :data:`EXHAUSTED`."""
-        t, d = self.times, self.ic_delay
-        while self.pos + 1 < len(t) and t[self.pos + 1] - t[self.pos] < d:
-            self.pos += 2
-            self.filtered += 1
-        return EXHAUSTED if self.pos >= len(t) else int(t[self.pos]) + d
+        """Arrival time of the pin's next surviving toggle, or
+        :data:`EXHAUSTED`."""
+        self._drop_narrow_pairs()
+        if self.pos < len(self.times):
+            return int(self.times[self.pos]) + self.ic_delay
+        return EXHAUSTED
 
     def consume(self):
         self.pos += 1
@@ -67,14 +74,14 @@ class PinCursor:
 
 
 def next_event_time(cursors):
-    """Earliest pending delayed transition over all pins (time only)."""
-    pending = [t for t in (c.peek() for c in cursors) if t is not EXHAUSTED]
-    return min(pending) if pending else EXHAUSTED
+    """Earliest pending arrival over all pins (the time only)."""
+    arrivals = [t for t in map(PinCursor.peek, cursors) if t is not EXHAUSTED]
+    return min(arrivals, default=EXHAUSTED)
 
 
 def resolve_msi(cursors, t):
-    """Consume every pin transition landing exactly at ``t``; returns the
-    post-transition input vector and the switching pin indices."""
+    """Apply every arrival at exactly ``t`` (multiple simultaneous inputs);
+    returns the input vector after them and the switching pin indices."""
     switching = [p for p, c in enumerate(cursors) if c.peek() == t]
     for p in switching:
         cursors[p].consume()
@@ -97,65 +104,76 @@ class GateSimState:
     last_stored: bool = False
     out_times: list = field(default_factory=list)
 
+    def previous_edge(self):
+        """The edge a new one is compared with: the newest edge (stored or
+        discarded), else the newest stored edge left after withdrawals."""
+        if self.t_last is not None:
+            return self.t_last
+        return self.out_times[-1] if self.out_times else None
+
+    def withdraw_previous(self):
+        """The new edge cancels the previous one: both vanish."""
+        if self.t_last is not None and not self.last_stored:
+            self.discarded -= 1          # it had been discarded, nothing stored
+        else:
+            self.out_times.pop()
+            self.tc -= 1
+        self.filtered += 1
+        self.t_last = None
+
+    def record(self, t_out, delay, window_end):
+        self.last_stored = t_out < window_end
+        if self.last_stored:
+            self.out_times.append(t_out)
+            self.tc += 1
+        else:
+            self.discarded += 1
+        self.t_last, self.d_last = t_out, delay
+
 
 def emit_output(state, new_y, t_event, delay, window_end):
     """Schedule an output edge through the inertial filter (``SC:117-160``).
 
-    The edge lands at ``t_event + delay``.  If that is at or before the newest
-    surviving edge, or closer to it than ``delay * pct // 100``, the pulse is
-    cancelled in full (the older edge is retracted, nothing is emitted, the
-    output returns to its pre-pulse value); after that the newest remaining
-    stored edge is the comparison target.  Edges at or past ``window_end`` are
-    discarded but still update the logical value.
+    The edge lands at ``t_event + delay``.  At or before the previous edge, or
+    closer to it than ``delay * pct // 100``, it withdraws that edge and is
+    not emitted (the output returns to its pre-pulse value); the newest
+    remaining stored edge is then the next comparison target.  Edges at or
+    past ``window_end`` are discarded but still set the logical value.
     """
     if new_y == state.y:
         return state
     t_out = t_event + delay
-    thr = delay * state.pathpulse_pct // 100
-    if state.t_last is not None:
-        target = state.t_last
+    prev = state.previous_edge()
+    if prev is not None and (t_out <= prev or t_out - prev < delay * state.pathpulse_pct // 100):
+        state.withdraw_previous()
     else:
-        target = state.out_times[-1] if state.out_times else None
-    if target is not None and (t_out <= target or t_out - target < thr):
-        if state.t_last is not None and not state.last_stored:
-            state.discarded -= 1
-        else:
-            state.out_times.pop()
-            state.tc -= 1
-        state.filtered += 1
-        state.t_last = None
-    else:
-        state.last_stored = t_out < window_end
-        if state.last_stored:
-            state.out_times.append(t_out)
-            state.tc += 1
-        else:
-            state.discarded += 1
-        state.t_last = t_out
-        state.d_last = delay
+        state.record(t_out, delay, window_end)
     state.y = new_y
     return state
+
+
+def _event_delay(arc_tables, k, switching, values, col):
+    """Delay of an output edge: the largest conditioned arc delay over the
+    switching pins (``SC:139-151``)."""
+    return max((int(arc_tables[p][condition_row(k, p, values), col]) for p in switching),
+               default=0)
 
 
 def simulate_gate_window(cell, pin_waveforms, ic_delays, arc_tables, window_end,
                          mode="store", pathpulse_pct=100):
     """One gate over one window from explicit fanin waveforms (``SC:163-197``)."""
-    cursors = [PinCursor.from_waveform(w, d) for w, d in zip(pin_waveforms, ic_delays)]
-    k = len(cursors)
-    state = GateSimState(y=eval_lut(cell, [c.value for c in cursors]), mode=mode,
+    pins = [PinCursor.from_waveform(w, d) for w, d in zip(pin_waveforms, ic_delays)]
+    state = GateSimState(y=eval_lut(cell, [c.value for c in pins]), mode=mode,
                          pathpulse_pct=pathpulse_pct)
-    while True:
-        t = next_event_time(cursors)
-        if t is EXHAUSTED:
-            break
-        values, switching = resolve_msi(cursors, t)
-        ny = eval_lut(cell, values)
-        if ny != state.y:
-            col = 0 if ny else 1
-            delay = max([int(arc_tables[p][condition_row(k, p, values), col])
-                         for p in switching] + [0])
-            emit_output(state, ny, t, delay, window_end)
-    state.ic_filtered = sum(c.filtered for c in cursors)
+    t = next_event_time(pins)
+    while t is not EXHAUSTED:
+        values, switching = resolve_msi(pins, t)
+        y = eval_lut(cell, values)
+        if y != state.y:
+            emit_output(state, y, t, _event_delay(arc_tables, len(pins), switching, values,
+                                                  0 if y else 1), window_end)
+        t = next_event_time(pins)
+    state.ic_filtered = sum(c.filtered for c in pins)
     return state
 
 
