@@ -781,9 +781,12 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         const unsigned aT = aL + ((nT + kWarp - 1) & ~(unsigned)(kWarp - 1));
         GS_PROF_ADD(PF_LOOP_WINDOWS, warp == 0 ? nL : 0);
         GS_PROF_ADD(PF_TRIVIAL, warp == 0 ? nT : 0);
-        // one index space [0, aT + nS) dealt to the threads round robin;
-        // each list walked by its own loop from the thread's first index in
-        // the list's range
+        // loop windows: one per thread from warp 0 up (the whole CTA round
+        // robin when there are more than its threads); two- and single-
+        // transition windows (one index space, the singles after the
+        // warp-aligned twos) dealt round robin over the warps left without
+        // loop windows, so the long event loops and the short windows finish
+        // together at the barrier
         const unsigned ut = (unsigned)tid;
         for (unsigned i = ut; i < nL; i += kLeanThreads) {
           const unsigned e = S.s.list[i];
@@ -795,15 +798,26 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
             loop_window<MODE, K, PCT100, false, SLAB>(C, g, lut, ic, A.pct, S.s.dtab, Tw,
                                                       (int)(e & 127u), (e >> 7) & 15u, acc);
         }
-        for (unsigned i = aL + ((ut - aL) & (kLeanThreads - 1)); i < aL + nT; i += kLeanThreads) {
-          const unsigned e = S.s.list[kPool + i - aL];
-          two_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, S.s.ic, A.pct, S.s.dtab, S.w[e >> 11],
-                                            (int)(e & 127u), (e >> 7) & 15u, acc);
-        }
-        for (unsigned i = aT + ((ut - aT) & (kLeanThreads - 1)); i < aT + nS; i += kLeanThreads) {
-          const unsigned e = S.s.list[2 * kPool + i - aT];
-          single_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, S.s.ic, S.s.dtab, S.w[e >> 11],
-                                               (int)(e & 127u), (e >> 7) & 15u, acc);
+        const unsigned loop_warps = aL / kWarp;
+        const bool spare = loop_warps < (unsigned)kLeanWarps;
+        const unsigned first = spare ? loop_warps * kWarp : 0u;  // first thread of the deal
+        const unsigned nth = kLeanThreads - first;
+        const unsigned aT2 = (nT + kWarp - 1) & ~(unsigned)(kWarp - 1);
+        if (ut >= first) {
+          for (unsigned i = ut - first; i < aT2 + nS; i += nth) {
+            if (i < aT2) {
+              if (i < nT) {
+                const unsigned e = S.s.list[kPool + i];
+                two_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, S.s.ic, A.pct, S.s.dtab,
+                                                  S.w[e >> 11], (int)(e & 127u), (e >> 7) & 15u,
+                                                  acc);
+              }
+            } else {
+              const unsigned e = S.s.list[2 * kPool + i - aT2];
+              single_window<MODE, K, PCT100, SLAB>(C, g, lut, ic, S.s.ic, S.s.dtab, S.w[e >> 11],
+                                                   (int)(e & 127u), (e >> 7) & 15u, acc);
+            }
+          }
         }
       }
       GS_PROF_T(pt2);
