@@ -676,16 +676,23 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         const bool in_smem = inw + UB <= (unsigned)SLAB;
         unsigned *stage;
         if (in_smem) {
-          if (inw && lane == 0) {
-            fence_proxy_async();  // the slab's earlier generic accesses before the async writes
-            mbar_expect_tx(&T.mbar, inw * 4u);
+          if (inw && lane < (unsigned)K) {
+            // lane p issues pin p's copy (the mbarrier's transaction count
+            // may run ahead of lane 0's expect, PTX: -(2^20-1) .. 2^20-1)
+            unsigned tp = tot[0], sp = seg[0];
+            unsigned long long bp = tb[0];
 #pragma unroll
-            for (int p = 0; p < K; ++p)
-              if (tot[p]) {
-                const unsigned sh = (unsigned)tb[p] & 3u;
-                bulk_g2s(&T.slab[seg[p] - sh], data + (tb[p] - sh),
-                         ((sh + tot[p] + 3u) & ~3u) * 4u, &T.mbar);
-              }
+            for (int p = 1; p < K; ++p) {
+              tp = lane == (unsigned)p ? tot[p] : tp;
+              sp = lane == (unsigned)p ? seg[p] : sp;
+              bp = lane == (unsigned)p ? tb[p] : bp;
+            }
+            fence_proxy_async();  // the slab's earlier generic accesses before the async writes
+            if (lane == 0) mbar_expect_tx(&T.mbar, inw * 4u);
+            if (tp) {
+              const unsigned sh = (unsigned)bp & 3u;
+              bulk_g2s(&T.slab[sp - sh], data + (bp - sh), ((sh + tp + 3u) & ~3u) * 4u, &T.mbar);
+            }
           }
           // staged statistics runs address the slab by offset (stage_at);
           // no generic pointer is formed
