@@ -725,10 +725,12 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         // read in place send every window with a transition to the loop list.
         // Positions: one warp scan of the lane's packed class counts, one
         // shared-memory atomic for all three lists of the warp.
+        // the lane's windows inside the chunk: j < nv
+        const int nv = ok ? min(max(nact - wl, 0), kWPL) : 0;
         unsigned cls[kWPL], V = 0;
 #pragma unroll
         for (int j = 0; j < kWPL; ++j) {
-          const bool a = ok && wl + j < nact;
+          const bool a = j < nv;
           const unsigned m = in_smem ? min(n[j], 3u) : (n[j] ? 3u : 0u);
           cls[j] = a ? m : 0u;
           V += (1u << (kListBits * cls[j])) >> kListBits;
@@ -759,7 +761,7 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         load_counts(C.wlen32 + base_w + wl, wl4);
 #pragma unroll
         for (int j = 0; j < kWPL; ++j) {
-          const bool act = ok && wl + j < nact;
+          const bool act = j < nv;
           const unsigned y0 = (unsigned)(lut >> ix[j]) & 1u;
           const bool quiet = act && n[j] == 0;
           acc.t1 += (quiet && y0) ? wl4[j] : 0u;
@@ -833,9 +835,7 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
       // ---- (C) compaction of this warp's tile and the per-net sums
       if (tile) {
         unsigned co[kWPL], so[kWPL], s = 0;
-        unsigned amask = 0;
-#pragma unroll
-        for (int j = 0; j < kWPL; ++j) amask |= (ok && wl + j < nact ? 1u : 0u) << j;
+        const unsigned amask = (1u << (ok ? min(max(nact - wl, 0), kWPL) : 0)) - 1u;
         ld4(&T.cnt[wl], co);
         ld4(&T.offs[0][wl], so);
 #pragma unroll
