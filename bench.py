@@ -47,7 +47,8 @@ def parse_args():
     ap.add_argument("--config", default="", help="C2/C3/C4/C5-... (default C3 at N=1, C4 at N>1)")
     ap.add_argument("--windows", type=int, default=0, help="windows per GPU (0 = the config's)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=0,
+                    help="end-to-end steps (0 = as many as --steps)")
     ap.add_argument("--cpu-windows", type=int, default=0,
                     help="CPU baseline / parity sample windows (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -394,7 +395,7 @@ def main():
         # from a worker thread) overlaps step i's simulation; every step still
         # uploads its inputs and reads its sums back inside the timed region
         from concurrent.futures import ThreadPoolExecutor
-        K = max(1, args.e2e_steps)
+        K = max(1, args.e2e_steps or args.steps)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
