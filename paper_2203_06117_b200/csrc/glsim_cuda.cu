@@ -881,7 +881,9 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
       }
       // ---- K1
       if (s->P > 0) {
-        const int tpi = std::max(1, std::min(Tc, 4));
+        // tiles per item: the CSR kernel searches once per item and carries
+        // the cut from tile to tile
+        const int tpi = std::max(1, std::min(Tc, s->csr ? 16 : 4));
         const int ntg = (Tc + tpi - 1) / tpi;
         const int64_t items = (int64_t)s->P * ntg;
         if (s->csr) {

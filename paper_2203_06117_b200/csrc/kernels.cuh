@@ -372,10 +372,29 @@ __global__ void __launch_bounds__(256) stim_segment_csr(StimDev S, ChunkDev C, i
     const unsigned init = S.pi_init[p];
     long long tc = 0, t1 = 0;
     const int t_hi = min((tg + 1) * tpi, C.Tc);
+    long long cut = -1;  // the tile's first toggle: searched once per item, then carried
     for (int t = tg * tpi; t < t_hi; ++t) {
       const int wl = t * kTile + (int)lane * kWPL;   // lane's first window (chunk-relative)
-      long long i = lower_bound(seg, n, wl < C.Wc ? C.bnd[C.w0 + wl] : b_end);
-      const long long cut0 = __shfl_sync(0xffffffffu, i, 0);
+      const int wt = t * kTile;
+      if (cut < 0) cut = lower_bound(seg, n, wt < C.Wc ? C.bnd[C.w0 + wt] : b_end);
+      const long long cut0 = cut;
+      // the lane's first toggle: cut0 + the tile's toggles before the lane's
+      // first window, counted 32 at a time from coalesced loads (the toggles
+      // ascend over the lanes: a shuffle binary search per round)
+      const long long bl = wl < C.Wc ? C.bnd[C.w0 + wl] : b_end;
+      const long long b_t1 = wt + kTile < C.Wc ? C.bnd[C.w0 + wt + kTile] : b_end;
+      long long i = cut0;
+      for (long long base = cut0;; base += kWarp) {
+        const long long k = base + lane;
+        const long long x = k < n ? __ldg(seg + k) : LLONG_MAX;
+        int pos = 0;
+#pragma unroll
+        for (int st = kWarp / 2; st > 0; st >>= 1)
+          pos += __shfl_sync(0xffffffffu, x, pos + st - 1) < bl ? st : 0;
+        pos += __shfl_sync(0xffffffffu, x, pos) < bl ? 1 : 0;
+        i += pos;
+        if (!(__shfl_sync(0xffffffffu, x, kWarp - 1) < b_t1)) break;
+      }
       unsigned c[kWPL];
       unsigned nib = 0;
 #pragma unroll
@@ -406,6 +425,7 @@ __global__ void __launch_bounds__(256) stim_segment_csr(StimDev S, ChunkDev C, i
       store_counts(C.cnt + (size_t)p * C.Wpad + wl, c, true);
       if (lane == 0) C.tbase[(size_t)p * C.Tc + t] = (unsigned long long)(off + cut0);
       store_init_words(C.init + (size_t)p * Tw, t, nib);
+      cut = __shfl_sync(0xffffffffu, i, kWarp - 1);  // the next tile's first toggle
     }
     acc_flush(C, p, t1, tc, 0, 0, 0);
   }

@@ -19,7 +19,10 @@ for l in open("gpurun_out/ab_lean.jsonl"):
     except Exception:
         continue
     r = x["run"]
-    d[(x["variant"], r["config"]["workload"][:2])].append(r["roofline"]["k4_ms_per_step"])
+    d[(x["variant"], r["config"]["workload"][:2])].append((r["roofline"]["k4_ms_per_step"], r["ms_per_step"]))
 for k, v in sorted(d.items()):
-    print(k, "k4 ms", [round(a, 2) for a in v], "median", round(statistics.median(v), 2))
+    k4 = [a for a, _ in v]
+    st = [b for _, b in v]
+    print(k, "k4 ms", [round(a, 2) for a in k4], "median", round(statistics.median(k4), 2),
+          "| step ms median", round(statistics.median(st), 2))
 PY
