@@ -577,6 +577,10 @@ int launch_lean(int sms, cudaStream_t st, const DesignDev &Dd, const ChunkDev &C
   return GS_OK;
 }
 
+#ifndef GS_META_PCT
+#define GS_META_PCT 40  // share of the device budget for chunk metadata (dev A/B knob)
+#endif
+
 // largest persistent grid any kernel of a run may use (sizes the regions)
 template <typename TS, int MODE>
 int grid_size(gs_engine *e, bool narrow, bool p100, int *ncta) {
@@ -778,9 +782,10 @@ int run_chunks(gs_engine *e, gs_stim *s, int64_t w_lo, int64_t w_hi, int pct, Ru
   const int64_t pi_words = s->csr ? s->n_toggles : 0;
   const int64_t pi_bytes = round_up(pi_words * (int64_t)sizeof(TS), 256);
   const int64_t total = w_hi - w_lo;
-  // initial chunk: metadata takes at most ~40% of the budget (the hint of
-  // the last run of the same mode family may be smaller, never larger)
-  const int64_t meta_cap = std::max<int64_t>(kTile, (e->budget * 2 / 5) / per_win / kTile * kTile);
+  // initial chunk: metadata takes at most GS_META_PCT % of the budget (the
+  // hint of the last run of the same mode family may be smaller, never larger)
+  const int64_t meta_cap =
+      std::max<int64_t>(kTile, (e->budget / 100 * GS_META_PCT) / per_win / kTile * kTile);
   int64_t &hint = e->chunk_hint[arena ? 1 : 0];
   int64_t Wc = hint > 0 ? std::min(hint, meta_cap) : meta_cap;
   Wc = std::min<int64_t>(Wc, round_up(total, kTile));
