@@ -8,21 +8,25 @@
 //
 // One CTA = one gate x a super-tile of 4 consecutive 128-window tiles; warp i
 // owns tile i of it and lane l windows 4l .. 4l+3 of that tile.
-//   (A) per warp: per pin the tile's count row (one 16-byte load per lane)
-//       and a warp scan -> the lane's window offsets in the pin's segment;
-//       the pins' segments staged into the warp's shared-memory slab by one
-//       TMA bulk copy (cp.async.bulk, completion on an mbarrier) per pin,
-//       issued by one lane and overlapped with the classification.  Windows
-//       with no input transition (the output keeps its window-start value)
-//       or exactly one are finished by the lane that owns them -- Algo. 1
-//       with a single event is one LUT lookup, one delay lookup and one
-//       window-end test (_kernels.py:94-203, one iteration).  Windows with
-//       more transitions go to the CTA's worklists;
+//   (A) per warp: per pin the tile's count row (prefetched by cp.async
+//       during the previous tile) and warp scans (two pins per scan) -> the
+//       lane's window offsets in the pin's segment; the window-start input
+//       vectors by a 4x4 bit transpose; the pins' segments staged into the
+//       warp's shared-memory slab by one TMA bulk copy (cp.async.bulk,
+//       completion on an mbarrier) per pin, each issued by its own lane and
+//       overlapped with the classification.  Windows with no input
+//       transition keep their window-start value and are finished by the
+//       lane that owns them; the others go to the CTA's worklists by class
+//       (one, two, three or more transitions), positioned by one warp scan
+//       of the lane's packed class counts and one shared-memory atomic;
 //   (M) the whole CTA works the pooled lists of its 4 tiles, so the few busy
-//       windows of each tile fill whole warps: two transitions in closed form
-//       (the interconnect pair filter of a same-pin pair, _kernels.py:96-117,
-//       included), three or more through sim_span's event loop with its lazy
-//       interconnect filter;
+//       windows of each tile fill whole warps: three or more transitions
+//       through sim_span's event loop with its lazy interconnect filter
+//       (the loop windows take the first warps), two in closed form (the
+//       interconnect pair filter of a same-pin pair, _kernels.py:96-117,
+//       included) and one as a single Algo. 1 step (_kernels.py:94-203, one
+//       iteration) -- these two dealt over the warps without loop windows,
+//       so the warps reach the barrier together;
 //   (C) per warp: warp scan of the output counts, one pool allocation, the
 //       outputs copied out of the staging area; per-net dwell / toggle /
 //       filter sums.
