@@ -314,17 +314,36 @@ __device__ __forceinline__ void loop_window(const ChunkDev &C, int g, unsigned l
       const bool adv = (sw >> p) & 1u;
       unsigned q = cur[p] + (adv ? 1u : 0u);
       const unsigned d = ic[p];
-      if (d > 0) {  // the gate's pin: uniform across the CTA
-        bool narrow = adv && q + 1 < end[p] && at(p, q + 1) - at(p, q) < d;
-        while (narrow) {
-          q += 2;
-          ++icf;
-          narrow = q + 1 < end[p] && at(p, q + 1) - at(p, q) < d;
+      if constexpr (SMEM) {
+        // staged: both candidate toggles loaded unconditionally (a cursor at
+        // most two words past the segment still reads inside the warp's
+        // shared-memory slice), so no pin takes a divergent branch
+        unsigned t0 = T.slab[q], t1 = T.slab[q + 1];
+        if (d > 0) {  // the gate's pin: uniform across the CTA
+          bool narrow = adv && q + 1 < end[p] && t1 - t0 < d;
+          while (narrow) {
+            q += 2;
+            ++icf;
+            t0 = T.slab[q];
+            t1 = T.slab[q + 1];
+            narrow = q + 1 < end[p] && t1 - t0 < d;
+          }
         }
+        cur[p] = q;
+        nxt[p] = adv ? (q < end[p] ? t0 + d : INF) : nxt[p];
+      } else {
+        if (d > 0) {
+          bool narrow = adv && q + 1 < end[p] && at(p, q + 1) - at(p, q) < d;
+          while (narrow) {
+            q += 2;
+            ++icf;
+            narrow = q + 1 < end[p] && at(p, q + 1) - at(p, q) < d;
+          }
+        }
+        cur[p] = q;
+        const unsigned v = adv && q < end[p] ? at(p, q) + d : INF;
+        nxt[p] = adv ? v : nxt[p];
       }
-      cur[p] = q;
-      const unsigned v = adv && q < end[p] ? at(p, q) + d : INF;
-      nxt[p] = adv ? v : nxt[p];
     }
     // output side (K:136-193)
     const unsigned ny = (unsigned)(lut >> idx) & 1u;
