@@ -274,14 +274,30 @@ __device__ __forceinline__ void loop_window(const ChunkDev &C, int g, unsigned l
   auto refresh = [&](int p) {
     unsigned q = cur[p];
     const unsigned d = ic[p];
-    if (d > 0) {
-      while (q + 1 < end[p] && at(p, q + 1) - at(p, q) < d) {
-        q += 2;
-        ++icf;
+    if constexpr (SMEM) {  // unconditional slab loads, as in the event loop
+      unsigned t0 = T.slab[q], t1 = T.slab[q + 1];
+      if (d > 0) {
+        bool narrow = q + 1 < end[p] && t1 - t0 < d;
+        while (narrow) {
+          q += 2;
+          ++icf;
+          t0 = T.slab[q];
+          t1 = T.slab[q + 1];
+          narrow = q + 1 < end[p] && t1 - t0 < d;
+        }
+        cur[p] = q;
       }
-      cur[p] = q;
+      nxt[p] = q < end[p] ? t0 + d : INF;
+    } else {
+      if (d > 0) {
+        while (q + 1 < end[p] && at(p, q + 1) - at(p, q) < d) {
+          q += 2;
+          ++icf;
+        }
+        cur[p] = q;
+      }
+      nxt[p] = q < end[p] ? at(p, q) + d : INF;
     }
-    nxt[p] = q < end[p] ? at(p, q) + d : INF;
   };
 #pragma unroll
   for (int p = 0; p < K; ++p) {
