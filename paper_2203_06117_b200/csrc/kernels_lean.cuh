@@ -897,24 +897,14 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         // with more take a loop.  Staged statistics tiles read the slab with
         // shared-memory addressing, the others the generic staging pointer.
         auto copy_out = [&](const unsigned *stage) {
+          // the lane's outputs as one flat run: output q of the lane comes
+          // from window j (the last with cum[j] <= q) at so[j] + q - cum[j]
           unsigned *dst = data + ob + cx;
-          unsigned o = 0;
-          bool big = false;
-#pragma unroll
-          for (int j = 0; j < kWPL; ++j) {
-            const unsigned *sp = stage + so[j];
-            if (co[j] >= 1) dst[o] = sp[0];
-            if (co[j] >= 2) dst[o + 1] = sp[1];
-            big |= co[j] > 2;
-            o += co[j];
-          }
-          if (__any_sync(0xffffffffu, big)) {
-            o = 0;
-#pragma unroll
-            for (int j = 0; j < kWPL; ++j) {
-              for (unsigned q = 2; q < co[j]; ++q) dst[o + q] = stage[so[j] + q];
-              o += co[j];
-            }
+          const unsigned c1 = co[0], c2 = c1 + co[1], c3 = c2 + co[2];
+          const unsigned d0 = so[0], d1 = so[1] - c1, d2 = so[2] - c2, d3 = so[3] - c3;
+          for (unsigned q = 0; q < s; ++q) {
+            const unsigned d = q >= c3 ? d3 : q >= c2 ? d2 : q >= c1 ? d1 : d0;
+            dst[q] = stage[d + q];
           }
         };
         if (wrote) {
