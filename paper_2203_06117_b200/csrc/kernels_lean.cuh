@@ -902,6 +902,7 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
           unsigned *dst = data + ob + cx;
           const unsigned c1 = co[0], c2 = c1 + co[1], c3 = c2 + co[2];
           const unsigned d0 = so[0], d1 = so[1] - c1, d2 = so[2] - c2, d3 = so[3] - c3;
+#pragma unroll 2
           for (unsigned q = 0; q < s; ++q) {
             const unsigned d = q >= c3 ? d3 : q >= c2 ? d2 : q >= c1 ? d1 : d0;
             dst[q] = stage[d + q];
