@@ -776,8 +776,15 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         }
         unsigned VT;
         unsigned P = warp_excl_scan(V, &VT);
-        unsigned base = 0;
-        if (lane == 0 && VT) base = atomicAdd(&S.s.nlist[par], VT);
+        // lane 0's shared-memory atomic as a predicated instruction (no
+        // branch); the other lanes' result register is never read
+        unsigned base;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, 0;\n\t"
+            "@p atom.shared.add.u32 %0, [%2], %3;\n\t}"
+            : "=r"(base)
+            : "r"(lane), "r"(smem_addr(&S.s.nlist[par])), "r"(VT)
+            : "memory");
         P += __shfl_sync(0xffffffffu, base, 0);
         // every window stores (no branch): quiet ones into the thread's sink slot
         unsigned short *lists = S.s.list;
