@@ -325,41 +325,77 @@ __device__ __forceinline__ void loop_window(const ChunkDev &C, int g, unsigned l
     idx ^= sw;
     // the switching pins advance: predicated per pin (no divergent branch);
     // only a narrow pair (rare) enters the filter loop
+    auto advance_pins = [&]() {
 #pragma unroll
-    for (int p = 0; p < K; ++p) {
-      const bool adv = (sw >> p) & 1u;
-      unsigned q = cur[p] + (adv ? 1u : 0u);
-      const unsigned d = ic[p];
-      if constexpr (SMEM) {
-        // staged: both candidate toggles loaded unconditionally (a cursor at
-        // most two words past the segment still reads inside the warp's
-        // shared-memory slice), so no pin takes a divergent branch
-        unsigned t0 = T.slab[q], t1 = T.slab[q + 1];
-        if (d > 0) {  // the gate's pin: uniform across the CTA
-          bool narrow = adv && q + 1 < end[p] && t1 - t0 < d;
-          while (narrow) {
-            q += 2;
-            ++icf;
-            t0 = T.slab[q];
-            t1 = T.slab[q + 1];
-            narrow = q + 1 < end[p] && t1 - t0 < d;
+      for (int p = 0; p < K; ++p) {
+        const bool adv = (sw >> p) & 1u;
+        unsigned q = cur[p] + (adv ? 1u : 0u);
+        const unsigned d = ic[p];
+        if constexpr (SMEM) {
+          // staged: both candidate toggles loaded unconditionally (a cursor at
+          // most two words past the segment still reads inside the warp's
+          // shared-memory slice), so no pin takes a divergent branch
+          unsigned t0 = T.slab[q], t1 = T.slab[q + 1];
+          if (d > 0) {  // the gate's pin: uniform across the CTA
+            bool narrow = adv && q + 1 < end[p] && t1 - t0 < d;
+            while (narrow) {
+              q += 2;
+              ++icf;
+              t0 = T.slab[q];
+              t1 = T.slab[q + 1];
+              narrow = q + 1 < end[p] && t1 - t0 < d;
+            }
           }
-        }
-        cur[p] = q;
-        nxt[p] = adv ? (q < end[p] ? t0 + d : INF) : nxt[p];
-      } else {
-        if (d > 0) {
-          bool narrow = adv && q + 1 < end[p] && at(p, q + 1) - at(p, q) < d;
-          while (narrow) {
-            q += 2;
-            ++icf;
-            narrow = q + 1 < end[p] && at(p, q + 1) - at(p, q) < d;
+          cur[p] = q;
+          nxt[p] = adv ? (q < end[p] ? t0 + d : INF) : nxt[p];
+        } else {
+          if (d > 0) {
+            bool narrow = adv && q + 1 < end[p] && at(p, q + 1) - at(p, q) < d;
+            while (narrow) {
+              q += 2;
+              ++icf;
+              narrow = q + 1 < end[p] && at(p, q + 1) - at(p, q) < d;
+            }
           }
+          cur[p] = q;
+          const unsigned v = adv && q < end[p] ? at(p, q) + d : INF;
+          nxt[p] = adv ? v : nxt[p];
         }
-        cur[p] = q;
-        const unsigned v = adv && q < end[p] ? at(p, q) + d : INF;
-        nxt[p] = adv ? v : nxt[p];
       }
+    };
+    if constexpr (SMEM && K >= 3) {
+      // one switching pin (the common case): its cursor fetched by selects,
+      // advanced once, written back -- instead of K predicated advances
+      if ((sw & (sw - 1u)) == 0u) {
+        const unsigned ps = (unsigned)__ffs(sw) - 1u;
+        unsigned q = cur[0], e = end[0], d = ic[0];
+#pragma unroll
+        for (int k = 1; k < K; ++k) {
+          q = ps == (unsigned)k ? cur[k] : q;
+          e = ps == (unsigned)k ? end[k] : e;
+          d = ps == (unsigned)k ? ic[k] : d;
+        }
+        q += 1;
+        unsigned t0 = T.slab[q], t1 = T.slab[q + 1];
+        bool narrow = d > 0 && q + 1 < e && t1 - t0 < d;
+        while (narrow) {
+          q += 2;
+          ++icf;
+          t0 = T.slab[q];
+          t1 = T.slab[q + 1];
+          narrow = q + 1 < e && t1 - t0 < d;
+        }
+        const unsigned nv = q < e ? t0 + d : INF;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          cur[k] = ps == (unsigned)k ? q : cur[k];
+          nxt[k] = ps == (unsigned)k ? nv : nxt[k];
+        }
+      } else {
+        advance_pins();
+      }
+    } else {
+      advance_pins();
     }
     // output side (K:136-193)
     const unsigned ny = (unsigned)(lut >> idx) & 1u;
