@@ -803,10 +803,11 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
         // the lane's windows inside the chunk: j < nv
         const int nv = ok ? min(max(nact - wl, 0), kWPL) : 0;
         unsigned cls[kWPL], V = 0;
+        const unsigned mul = in_smem ? 1u : 3u;  // in place: every active window loops
 #pragma unroll
         for (int j = 0; j < kWPL; ++j) {
           const bool a = j < nv;
-          const unsigned m = in_smem ? min(n[j], 3u) : (n[j] ? 3u : 0u);
+          const unsigned m = min(n[j] * mul, 3u);
           cls[j] = a ? m : 0u;
           V += (1u << (kListBits * cls[j])) >> kListBits;
         }
