@@ -257,7 +257,7 @@ __device__ __forceinline__ void prefetch_tile(const ChunkDev &C, const int (&net
 // sim_span's refresh does (_kernels.py:96-117).  Outputs go to the tile's
 // staging area at the window's slot.
 template <int MODE, int K, bool PCT100, bool SMEM, int SLAB>
-__device__ __forceinline__ void loop_window(const ChunkDev &C, int g, unsigned long long lut,
+__device__ __forceinline__ void loop_window(const ChunkDev &C, int g, unsigned lut,
                                             const unsigned (&ic)[K], int pct,
                                             const unsigned *dtab, LeanWarp<K, SLAB> &T, int w,
                                             unsigned idx, LeanAcc &acc) {
@@ -472,7 +472,7 @@ __device__ __forceinline__ void loop_window(const ChunkDev &C, int g, unsigned l
 // iteration) -- one LUT lookup, one delay lookup, one window-end test.  Only
 // staged tiles classify windows as single.
 template <int MODE, int K, bool PCT100, int SLAB>
-__device__ __forceinline__ void single_window(const ChunkDev &C, int g, unsigned long long lut,
+__device__ __forceinline__ void single_window(const ChunkDev &C, int g, unsigned lut,
                                               const unsigned (&ic)[K], const unsigned *ic_of,
                                               const unsigned *dtab,
                                               LeanWarp<K, SLAB> &T, int w, unsigned i0,
@@ -517,7 +517,7 @@ __device__ __forceinline__ void single_window(const ChunkDev &C, int g, unsigned
 // pins when the two transitions coincide) can only emit; event 2 can emit,
 // cancel event 1's edge, or leave it pending; no stored edge can be popped.
 template <int MODE, int K, bool PCT100, int SLAB>
-__device__ __forceinline__ void two_window(const ChunkDev &C, int g, unsigned long long lut,
+__device__ __forceinline__ void two_window(const ChunkDev &C, int g, unsigned lut,
                                            const unsigned (&ic)[K], const unsigned *ic_of,
                                            int pct, const unsigned *dtab, LeanWarp<K, SLAB> &T,
                                            int w, unsigned i0, LeanAcc &acc) {
@@ -631,7 +631,8 @@ gate_eval_lean(DesignDev D, ChunkDev C, LevelArgs A) {
     const int g = __ldg(D.order + A.lo + jg);
     const int gnet = D.P + g;
     const int pin0 = __ldg(D.gate_pin + g);
-    const unsigned long long lut = __ldg(D.gate_lut + g);
+    // the truth table of a k <= 4 cell fits 16 bits: 32-bit shifts
+    const unsigned lut = (unsigned)__ldg(D.gate_lut + g);
     const int u_lo = in_head ? tg * A.tpi : A.ntg * A.tpi + tg * A.tpi2;
     const int u_hi = min(u_lo + (in_head ? A.tpi : A.tpi2), STc);
     int net[K], arc[K];
