@@ -46,9 +46,15 @@ namespace gs {
 #ifndef GS_LEAN_CTAS2
 #define GS_LEAN_CTAS2 8   // CTAs per SM of the k <= 2 instances (dev A/B knob)
 #endif
+#ifndef GS_LEAN_CTAS3
+#define GS_LEAN_CTAS3 7   // CTAs per SM of the k = 3 instances (dev A/B knob)
+#endif
+#ifndef GS_LEAN_CTAS4
+#define GS_LEAN_CTAS4 6   // CTAs per SM of the k = 4 instances (dev A/B knob)
+#endif
 template <int K>
 __host__ __device__ constexpr int lean_ctas() {
-  return (K <= 2 ? GS_LEAN_CTAS2 : K == 3 ? 7 : 6) * 4 / GS_LEAN_WARPS;
+  return (K <= 2 ? GS_LEAN_CTAS2 : K == 3 ? GS_LEAN_CTAS3 : GS_LEAN_CTAS4) * 4 / GS_LEAN_WARPS;
 }
 
 constexpr int kLeanWarps = GS_LEAN_WARPS;
